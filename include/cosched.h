@@ -1,0 +1,199 @@
+/*
+ * cosched.h -- C-ABI of the B200-native exhaustive, model-driven co-location
+ * search of Arima et al., "Optimizing Hardware Resource Partitioning and Job
+ * Allocations on Modern GPUs under Power Caps" (arXiv 2405.03838).
+ *
+ * Citations: P:Lnnn = /root/reference/PAPER.md line (section / equation /
+ * table named beside it); R# = a reading of the paper listed in DESIGN.md.
+ *
+ * WHAT IT COMPUTES (one call chain per job queue):
+ *   For every set of n_slots jobs of the queue (pairs by default),
+ *   every partition state S of the caller's table and every power cap P of
+ *   the caller's grid (the search space of Table `search-space`, P:L556-566,
+ *   generalised per P:L500/L794), it evaluates the linear model
+ *       RPerf_i(S,P) = C(S,P).H(F_i) + sum_{j!=i} D(S,P).J(F_j)
+ *   with the basis H, J of Table `functions`, then
+ *       Throughput = sum_i RPerf_i, Fairness = min_i RPerf_i,
+ *   and keeps the config maximising Throughput (Problem 1) or
+ *   Throughput / P (Problem 2) subject to Fairness > alpha
+ *   (strict). That is the paper's exhaustive search run for
+ *   every set of a queue; the queue-level reductions (best set, best job ->
+ *   GPU allocation) are the extension of P:L843 (reading R12).
+ *
+ * All compute runs in the library's CUDA kernels (sm_100a). There is no CPU
+ * fallback: without a usable CUDA device every compute entry point returns
+ * COSCHED_E_CUDA.
+ *
+ * Conventions:
+ *  - Every function returns a cosched_status; no exception crosses the ABI.
+ *  - Validation happens before any launch; on error no output is modified and
+ *    cosched_last_error(h) holds a one-line message.
+ *  - "device" pointers are CUDA device (or managed) memory owned by the
+ *    caller; "host" pointers are ordinary host memory owned by the caller.
+ *  - Sets are unordered job tuples named by their colexicographic id:
+ *      pair   (j0<j1):      id = j1*(j1-1)/2 + j0
+ *      triple (j0<j1<j2):   id = C(j2,3) + C(j1,2) + j0
+ *      solo   (j0):         id = j0
+ *    where j are queue POSITIONS 0..n_jobs-1; slot i of the set gets j_i.
+ *  - Configs: c = state * n_caps + cap, state in table order, caps ascending.
+ *    Ties in the objective resolve to the lowest c (reading R9).
+ *  - Handles are not thread-safe. Collective calls (marked COLLECTIVE) must be
+ *    made by every rank of the communicator with identical arguments.
+ */
+#ifndef COSCHED_H
+#define COSCHED_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cosched_ctx* cosched_t;
+
+typedef enum {
+  COSCHED_OK = 0,
+  COSCHED_INFEASIBLE = 2,           /* non-fatal: nothing satisfies Fairness > alpha */
+  COSCHED_E_ARG = 10,               /* bad argument: null pointer, size, objective, alpha < 0, non-finite coefficient */
+  COSCHED_E_INVALID_ALLOCATION = 11, /* a state's GPCs < 1 or not summing to gpcs_total, memory option not 0/1,
+                                        caps not positive strictly ascending */
+  COSCHED_E_UNKNOWN_KEY = 12,       /* state_slice outside [0, n_slices) */
+  COSCHED_E_DEGENERATE_PROFILE = 13, /* a job has F1 <= 0.01 % (reading R4) */
+  COSCHED_E_RANGE = 14,             /* a counter is NaN/inf, outside [0,100], or F6+F7+F8 > 100 */
+  COSCHED_E_STATE = 15,             /* call order violated (e.g. best_set before score_all) */
+  COSCHED_E_CUDA = 20,              /* CUDA error or no CUDA device */
+  COSCHED_E_NCCL = 21,              /* NCCL missing or failed */
+  COSCHED_E_OOM = 22                /* workspace too small */
+} cosched_status;
+
+/* The searched space and the fitted model (all host pointers; deep-copied by
+ * cosched_create, the caller may free them on return). */
+typedef struct {
+  int32_t n_slots;            /* jobs per set: 1 solo, 2 pairs, 3 triples ("up to two" in the paper) */
+  int32_t gpcs_total;         /* every state's GPC counts sum to this: 7 on A100 under MIG, 8 B200-like */
+  int32_t n_states;           /* partition states S, in canonical (= tie-break) order */
+  const int32_t* state_gpcs;  /* [n_states][n_slots] GPCs given to each slot, each >= 1 (validation only) */
+  const int32_t* state_mem;   /* [n_states] LLC/HBM option: 0 shared, 1 private */
+  const int32_t* state_slice; /* [n_states][n_slots] coefficient row used by each slot (reading R1) */
+  int32_t n_slices;           /* rows of the coefficient table per cap */
+  int32_t n_caps;             /* power caps P */
+  const float* caps_w;        /* [n_caps] watts, > 0, strictly ascending */
+  const float* coef_c;        /* [n_caps][n_slices][6]  C of P:L458 (scalability) */
+  const float* coef_d;        /* [n_caps][n_slices][3]  D of P:L458 (interference) */
+  int32_t objective;          /* 1 = Problem 1 (Throughput; pass a one-cap grid for "given P"), 2 = Problem 2 (Throughput/P) */
+  float alpha;                /* fairness threshold, >= 0; feasible iff Fairness > alpha */
+} cosched_desc;
+
+/* Per-set results of cosched_score_all for this rank's shard
+ * [first_set, first_set + n_sets). Device pointers, caller-owned; either may
+ * be NULL (then only the queue-level reductions are kept). obj[k] is the best
+ * objective of set first_set+k (-inf if no config is feasible); cfg[k] its
+ * config id (-1 if none). first_set / n_sets must equal cosched_shard_range. */
+typedef struct {
+  float* obj;
+  int32_t* cfg;
+  int64_t first_set;
+  int64_t n_sets;
+} cosched_out;
+
+/* Validate and deep-copy the description; bind to CUDA device `cuda_device`.
+ * Errors: E_ARG, E_INVALID_ALLOCATION, E_UNKNOWN_KEY, E_CUDA. */
+cosched_status cosched_create(const cosched_desc* desc, int cuda_device, cosched_t* out_handle);
+
+void cosched_destroy(cosched_t h);
+
+/* Per-handle message of the last error ("" if none). Valid until the next call on h. */
+const char* cosched_last_error(cosched_t h);
+
+/* Message for errors that happen before a handle exists (create). */
+const char* cosched_last_create_error(void);
+
+/* ---- multi-GPU (one process per GPU) -------------------------------------
+ * The search shards by contiguous set-id range (whole colex columns, i.e. a
+ * range of the largest job position) with no data-path exchange; the only
+ * exchanges are the argmax all-reduces of cosched_best_set /
+ * cosched_best_allocation, done with ncclAllReduce(u64, max) on the
+ * library's own communicator. NCCL is loaded at run time (dlopen
+ * "libnccl.so.2", the copy torch already loaded when present). */
+
+/* Rank 0: write a 128-byte ncclUniqueId to uid_out (host). E_NCCL if NCCL is unavailable. */
+cosched_status cosched_get_unique_id(void* uid_out);
+
+/* COLLECTIVE: create the communicator from rank 0's id (host, 128 bytes).
+ * nranks == 1 (uid may be NULL) resets to single-rank mode. */
+cosched_status cosched_set_comm(cosched_t h, const void* nccl_unique_id, int rank, int nranks);
+
+/* This rank's set range for a queue of n_jobs (host only, no CUDA). Rank r of
+ * W gets the sets whose largest position lies in [b_r, b_{r+1}), with b_r
+ * the smallest b such that C(b, n_slots) >= r * C(n_jobs, n_slots) / W. */
+cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets);
+
+/* Host-only helpers (no CUDA): number of sets, colex unranking of a set id
+ * into ascending queue positions pos[n_slots], and the packed argmax key
+ * used by every reduction: key = (ord(obj) << 32) | (0xFFFFFFFF - set_id'),
+ * ord = order-preserving float->u32 map, key 0 = infeasible. */
+int64_t cosched_n_sets(int64_t n_jobs, int32_t n_slots);
+cosched_status cosched_unrank(int64_t n_jobs, int32_t n_slots, int64_t set_id, int64_t* pos);
+uint64_t cosched_pack_key(float obj, int64_t set_id);
+void cosched_unpack_key(uint64_t key, float* obj, int64_t* set_id);
+
+/* Bytes of device workspace cosched_score_all needs for n_jobs. */
+cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes);
+
+/* Score every set of this rank's shard (async on `cuda_stream`, a
+ * cudaStream_t; NULL = legacy default stream).
+ *  features_dev: float [n_rows][8], counters F1..F8 in percent (Table `counters`)
+ *  jobs_dev:     int32 [n_jobs] row of each queue position, or NULL for row = position
+ *  n_rows:       rows of features_dev (validates jobs_dev)
+ *  workspace_dev: >= cosched_workspace_size bytes, 256-byte aligned
+ *  out:          host struct with device pointers (may be NULL)
+ * Steps (all kernels): validate features (E_RANGE / E_DEGENERATE_PROFILE for
+ * the first bad queue position, reported at the next synchronising call),
+ * basis H, J, projection onto C, D, per-set model evaluation, objective,
+ * fairness constraint, per-set argmax, per-shard argmax key. */
+cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t n_rows,
+                                 const int32_t* jobs_dev, int64_t n_jobs, void* workspace_dev,
+                                 size_t workspace_bytes, const cosched_out* out, void* cuda_stream);
+
+/* Synchronise the last score_all and return this rank's best set (no comm).
+ * *key is the packed key (0 if no feasible set). Reports deferred validation errors. */
+cosched_status cosched_local_best_key(cosched_t h, uint64_t* key);
+
+/* COLLECTIVE (when a communicator is set): the queue's best set = max over
+ * ranks of the packed key (ncclAllReduce u64 max), then its best config and
+ * objective, re-derived on the GPU by its owner... by every rank (the set is
+ * recomputed locally from its id; no further exchange).
+ * COSCHED_INFEASIBLE if no set has a feasible config. */
+cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj);
+
+/* The best config of one set of the last scored queue, evaluated on the GPU
+ * (any rank, any set, no comm). rperf: host float[n_slots] (may be NULL);
+ * throughput / fairness / obj: host (may be NULL). COSCHED_INFEASIBLE (cfg -1)
+ * if no config of that set is feasible. */
+cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, float* obj,
+                                   float* rperf, float* throughput, float* fairness);
+
+/* COLLECTIVE: job -> GPU allocation over the last scored queue (reading R12):
+ * choose k disjoint sets maximising the sum of per-set objectives.
+ *  - exact when k * n_slots == n_jobs and n_jobs <= 20 (pairs) / 15 (triples):
+ *    every partition of the queue into sets, enumerated lowest-free-job-first
+ *    with partners ascending; partitions containing an infeasible set are
+ *    skipped; ties -> first in that order;
+ *  - greedy otherwise: repeatedly take the feasible set with the largest
+ *    (obj, -set_id) whose jobs are all free (computed as parallel
+ *    locally-dominant rounds on the GPU), the first k taken.
+ * Requires score_all with out != NULL covering the shard.
+ * set_ids, cfgs: host arrays of >= k entries; *n_found = sets chosen, in
+ * order of formation (exact) or of decreasing key (greedy).
+ * COSCHED_INFEASIBLE if no (complete, for exact) allocation exists. */
+cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids, int32_t* cfgs,
+                                       double* total_obj, int32_t* n_found);
+
+/* Number of kernels the library launched since create (instrumentation for bench.py). */
+int64_t cosched_kernel_launches(cosched_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COSCHED_H */
