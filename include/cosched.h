@@ -124,10 +124,19 @@ cosched_status cosched_get_unique_id(void* uid_out);
  * nranks == 1 (uid may be NULL) resets to single-rank mode. */
 cosched_status cosched_set_comm(cosched_t h, const void* nccl_unique_id, int rank, int nranks);
 
+/* Shard view without a communicator: score as rank `rank` of `nranks` on this
+ * one device (collectives then reduce over this process only). Used to test
+ * the multi-GPU sharding on a single GPU ("fake ranks"). */
+cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks);
+
 /* This rank's set range for a queue of n_jobs (host only, no CUDA). Rank r of
  * W gets the sets whose largest position lies in [b_r, b_{r+1}), with b_r
  * the smallest b such that C(b, n_slots) >= r * C(n_jobs, n_slots) / W. */
 cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets);
+
+/* The same partition without a handle (host only): rank of nranks, sets of n_slots jobs. */
+cosched_status cosched_shard_range_for(int64_t n_jobs, int32_t n_slots, int32_t rank, int32_t nranks,
+                                       int64_t* first_set, int64_t* n_sets);
 
 /* Host-only helpers (no CUDA): number of sets, colex unranking of a set id
  * into ascending queue positions pos[n_slots], and the packed argmax key
@@ -189,6 +198,11 @@ cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, fl
  * COSCHED_INFEASIBLE if no (complete, for exact) allocation exists. */
 cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids, int32_t* cfgs,
                                        double* total_obj, int32_t* n_found);
+
+/* Select the pair scorer: 1 = tiled fast kernel (default), 0 = generic
+ * one-thread-per-set kernel (the simple reference the fast one is tested
+ * against). Env COSCHED_PAIR_KERNEL=generic selects 0 at create. */
+cosched_status cosched_set_variant(cosched_t h, int variant);
 
 /* Number of kernels the library launched since create (instrumentation for bench.py). */
 int64_t cosched_kernel_launches(cosched_t h);

@@ -1,0 +1,775 @@
+// api.cu -- host side of the C-ABI declared in include/cosched.h.
+//
+// Validation, shard ranges, workspace carving, stream ordering and the NCCL
+// communicator. Every arithmetic step of the method runs in the kernels of
+// kernels.cu / score_pairs.cu; this file only moves arguments, launches and
+// reads back the few bytes of each result.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "cosched_internal.h"
+
+using namespace cosched;
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (the copy torch already loaded when present).
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclMax = 2 };
+struct NcclApi {
+  bool tried = false;
+  void* lib = nullptr;
+  int (*getUniqueId)(ncclUniqueId*) = nullptr;
+  int (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load(std::string* why) {
+  if (!g_nccl.tried) {
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      g_nccl.getUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+      g_nccl.commInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+      g_nccl.allReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+      g_nccl.commDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+      g_nccl.getErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      if (g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy) g_nccl.lib = h;
+    }
+  }
+  if (!g_nccl.lib && why) *why = "libnccl.so.2 not loadable";
+  return g_nccl.lib != nullptr;
+}
+
+thread_local std::string g_create_error;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+struct cosched_ctx {
+  int device = 0;
+  int n_slots = 2;
+  int objective = 2;
+  SpaceParams sp{};
+  DeviceTables tb{};
+  std::string err;
+  int variant = 1;
+  int64_t launches = 0;
+  // small scratch owned by the handle (exact allocation, details)
+  float* d_small_obj = nullptr;      // [kSmallSets]
+  int32_t* d_small_cfg = nullptr;    // [kSmallSets]
+  unsigned long long* d_small_key = nullptr;  // [2]
+  int64_t* d_small_ids = nullptr;    // [64]
+  float* d_detail = nullptr;         // [kDetailRows][8]
+  int64_t* d_detail_ids = nullptr;   // [kDetailRows]
+  unsigned long long* h_pinned = nullptr;  // [8] pinned host readback
+  // last score_all
+  bool scored = false;
+  int64_t n_jobs = 0;
+  int64_t first = 0, n_sets = 0;
+  Workspace ws{};
+  float* out_obj = nullptr;
+  int32_t* out_cfg = nullptr;
+  cudaStream_t stream = nullptr;
+  // communicator
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int view_nranks = 1;  // shard view without comm (tests)
+  static constexpr int kSmallSets = 512;
+  static constexpr int kDetailRows = 8192;
+};
+
+namespace cosched {
+
+int64_t n_sets(int64_t n, int k) {
+  if (n < k || k < 1) return 0;
+  if (k == 1) return n;
+  if (k == 2) return n * (n - 1) / 2;
+  return n * (n - 1) / 2 * (n - 2) / 3;  // exact: n(n-1)/2 * (n-2) is divisible by 3
+}
+
+uint32_t ord_float(float f) {
+  uint32_t b;
+  memcpy(&b, &f, 4);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+float unord_float(uint32_t o) {
+  uint32_t b = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t np, int64_t n_sets_local, char* base,
+                        Workspace* ws) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = base ? base + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  size_t proj = (size_t)n_jobs * n_slices * np * sizeof(float);
+  Workspace w;
+  w.ka = (float*)take(proj);
+  w.kb = (float*)take(proj);
+  w.best_key = (unsigned long long*)take(8);
+  w.err = (unsigned long long*)take(8);
+  w.counters = (int64_t*)take(8 * 8);
+  w.job_key = (unsigned long long*)take((size_t)n_jobs * 8);
+  w.taken = (uint32_t*)take((size_t)n_jobs * 4);
+  w.picked = (unsigned long long*)take((size_t)n_jobs * 8 + 8);
+  w.alive = (int64_t*)take((size_t)n_sets_local * 8 + 8);
+  w.alive2 = (int64_t*)take((size_t)n_sets_local * 8 + 8);
+  w.bytes = off;
+  if (ws) *ws = w;
+  return off;
+}
+
+}  // namespace cosched
+
+// ---------------------------------------------------------------------------
+static cosched_status fail(cosched_t h, cosched_status st, const std::string& msg) {
+  if (h) h->err = msg;
+  return st;
+}
+
+static cosched_status cuda_fail(cosched_t h, cudaError_t e, const char* where) {
+  return fail(h, COSCHED_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+  } while (0)
+
+static cosched_status validate_desc(const cosched_desc* d, std::string* msg) {
+  char buf[256];
+  if (!d || d->n_slots < 1 || d->n_slots > kMaxSlots || d->n_states < 1 || d->n_states > kMaxStates ||
+      d->n_slices < 1 || d->n_slices > 32767 || d->n_caps < 1 || d->n_caps > kMaxCaps || !d->state_gpcs ||
+      !d->state_mem || !d->state_slice || !d->caps_w || !d->coef_c || !d->coef_d) {
+    *msg = "bad sizes (n_slots 1..3, n_states 1..128, n_caps 1..64) or null table";
+    return COSCHED_E_ARG;
+  }
+  if (d->objective != 1 && d->objective != 2) {
+    *msg = "objective must be 1 or 2";
+    return COSCHED_E_ARG;
+  }
+  if (!(d->alpha >= 0.0f) || isinf(d->alpha)) {
+    *msg = "alpha must be finite and >= 0";
+    return COSCHED_E_ARG;
+  }
+  for (int s = 0; s < d->n_states; s++) {
+    long sum = 0;
+    for (int i = 0; i < d->n_slots; i++) {
+      int g = d->state_gpcs[s * d->n_slots + i];
+      if (g < 1) {
+        snprintf(buf, sizeof buf, "state %d slot %d: %d GPCs < 1", s, i, g);
+        *msg = buf;
+        return COSCHED_E_INVALID_ALLOCATION;
+      }
+      sum += g;
+    }
+    if (sum != d->gpcs_total) {
+      snprintf(buf, sizeof buf, "state %d: GPCs sum to %ld, not %d", s, sum, d->gpcs_total);
+      *msg = buf;
+      return COSCHED_E_INVALID_ALLOCATION;
+    }
+    if (d->state_mem[s] != 0 && d->state_mem[s] != 1) {
+      snprintf(buf, sizeof buf, "state %d: memory option %d", s, d->state_mem[s]);
+      *msg = buf;
+      return COSCHED_E_INVALID_ALLOCATION;
+    }
+  }
+  for (int c = 0; c < d->n_caps; c++) {
+    float w = d->caps_w[c];
+    if (!(w > 0.0f) || isinf(w) || (c > 0 && !(w > d->caps_w[c - 1]))) {
+      snprintf(buf, sizeof buf, "cap %d: %g W not positive / strictly ascending", c, (double)w);
+      *msg = buf;
+      return COSCHED_E_INVALID_ALLOCATION;
+    }
+  }
+  for (int s = 0; s < d->n_states; s++)
+    for (int i = 0; i < d->n_slots; i++) {
+      int sl = d->state_slice[s * d->n_slots + i];
+      if (sl < 0 || sl >= d->n_slices) {
+        snprintf(buf, sizeof buf, "state %d slot %d: slice %d not in coefficient table", s, i, sl);
+        *msg = buf;
+        return COSCHED_E_UNKNOWN_KEY;
+      }
+    }
+  for (long t = 0; t < (long)d->n_caps * d->n_slices * 6; t++)
+    if (!isfinite(d->coef_c[t])) {
+      *msg = "non-finite C coefficient";
+      return COSCHED_E_ARG;
+    }
+  for (long t = 0; t < (long)d->n_caps * d->n_slices * 3; t++)
+    if (!isfinite(d->coef_d[t])) {
+      *msg = "non-finite D coefficient";
+      return COSCHED_E_ARG;
+    }
+  return COSCHED_OK;
+}
+
+extern "C" {
+
+const char* cosched_last_create_error(void) { return g_create_error.c_str(); }
+
+cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t* out_handle) {
+  g_create_error.clear();
+  if (!out_handle) {
+    g_create_error = "null out_handle";
+    return COSCHED_E_ARG;
+  }
+  *out_handle = nullptr;
+  std::string msg;
+  cosched_status st = validate_desc(d, &msg);
+  if (st != COSCHED_OK) {
+    g_create_error = msg;
+    return st;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev <= 0 || cuda_device < 0 || cuda_device >= ndev) {
+    g_create_error = std::string("no usable CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "index out of range");
+    return COSCHED_E_CUDA;
+  }
+  cosched_ctx* h = new cosched_ctx();
+  h->device = cuda_device;
+  h->n_slots = d->n_slots;
+  h->objective = d->objective;
+  SpaceParams& sp = h->sp;
+  sp.n_slots = d->n_slots;
+  sp.n_states = d->n_states;
+  sp.n_slices = d->n_slices;
+  sp.n_caps = d->n_caps;
+  sp.np = (d->n_caps + 3) & ~3;
+  sp.n_cfg = d->n_states * d->n_caps;
+  sp.alpha = d->alpha;
+  const float nalpha = (float)d->n_slots * d->alpha;
+  for (int p = 0; p < d->n_caps; p++) {
+    float inv = d->objective == 2 ? 1.0f / d->caps_w[p] : 1.0f;
+    sp.obj_scale[p] = inv * kInvScale;  // exact power-of-two rescale of fl(1/P)
+    sp.obj_bias[p] = nalpha * inv;
+  }
+  for (int s = 0; s < d->n_states; s++)
+    for (int i = 0; i < d->n_slots; i++) sp.slice[s][i] = (int16_t)d->state_slice[s * d->n_slots + i];
+  const char* v = getenv("COSCHED_PAIR_KERNEL");
+  if (v && !strcmp(v, "generic")) h->variant = 0;
+
+  DeviceGuard g(cuda_device);
+  size_t nc = (size_t)d->n_caps * d->n_slices;
+  bool ok = cudaMalloc(&h->tb.coef_c, nc * 6 * 4) == cudaSuccess &&
+            cudaMalloc(&h->tb.coef_d, nc * 3 * 4) == cudaSuccess &&
+            cudaMalloc(&h->d_small_obj, cosched_ctx::kSmallSets * 4) == cudaSuccess &&
+            cudaMalloc(&h->d_small_cfg, cosched_ctx::kSmallSets * 4) == cudaSuccess &&
+            cudaMalloc(&h->d_small_key, 2 * 8) == cudaSuccess &&
+            cudaMalloc(&h->d_small_ids, 64 * 8) == cudaSuccess &&
+            cudaMalloc(&h->d_detail, (size_t)cosched_ctx::kDetailRows * 8 * 4) == cudaSuccess &&
+            cudaMalloc(&h->d_detail_ids, (size_t)cosched_ctx::kDetailRows * 8) == cudaSuccess &&
+            cudaMallocHost(&h->h_pinned, 8 * 8) == cudaSuccess &&
+            cudaMemcpy(h->tb.coef_c, d->coef_c, nc * 6 * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemcpy(h->tb.coef_d, d->coef_d, nc * 3 * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (!ok) {
+    g_create_error = std::string("CUDA allocation/copy failed: ") + cudaGetErrorString(cudaGetLastError());
+    cosched_destroy(h);
+    return COSCHED_E_CUDA;
+  }
+  *out_handle = h;
+  return COSCHED_OK;
+}
+
+void cosched_destroy(cosched_t h) {
+  if (!h) return;
+  {
+    DeviceGuard g(h->device);
+    if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
+    cudaFree(h->tb.coef_c);
+    cudaFree(h->tb.coef_d);
+    cudaFree(h->d_small_obj);
+    cudaFree(h->d_small_cfg);
+    cudaFree(h->d_small_key);
+    cudaFree(h->d_small_ids);
+    cudaFree(h->d_detail);
+    cudaFree(h->d_detail_ids);
+    if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  }
+  delete h;
+}
+
+const char* cosched_last_error(cosched_t h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+int64_t cosched_kernel_launches(cosched_t h) { return h ? h->launches : 0; }
+
+cosched_status cosched_set_variant(cosched_t h, int variant) {
+  if (!h || variant < 0 || variant > 1) return COSCHED_E_ARG;
+  h->variant = variant;
+  return COSCHED_OK;
+}
+
+// ---- host-only helpers ------------------------------------------------------
+int64_t cosched_n_sets(int64_t n_jobs, int32_t n_slots) { return cosched::n_sets(n_jobs, n_slots); }
+
+cosched_status cosched_unrank(int64_t n_jobs, int32_t n_slots, int64_t set_id, int64_t* pos) {
+  if (!pos || n_slots < 1 || n_slots > 3 || set_id < 0 || set_id >= cosched::n_sets(n_jobs, n_slots))
+    return COSCHED_E_ARG;
+  int64_t rest = set_id;
+  for (int i = n_slots - 1; i >= 0; i--) {
+    // largest t with C(t, i+1) <= rest: binary search over [i, n_jobs)
+    int64_t lo = i, hi = n_jobs - 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi + 1) / 2;
+      if (cosched::n_sets(mid, i + 1) <= rest) lo = mid;
+      else hi = mid - 1;
+    }
+    pos[i] = lo;
+    rest -= cosched::n_sets(lo, i + 1);
+  }
+  return COSCHED_OK;
+}
+
+uint64_t cosched_pack_key(float obj, int64_t set_id) {
+  return ((uint64_t)ord_float(obj) << 32) | (0xFFFFFFFFull - (uint64_t)(uint32_t)set_id);
+}
+
+void cosched_unpack_key(uint64_t key, float* obj, int64_t* set_id) {
+  if (key == 0) {
+    if (obj) *obj = -INFINITY;
+    if (set_id) *set_id = -1;
+    return;
+  }
+  if (obj) *obj = unord_float((uint32_t)(key >> 32));
+  if (set_id) *set_id = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+}
+
+static void shard_bounds(int64_t n_jobs, int k, int rank, int nranks, int64_t* first, int64_t* count) {
+  int64_t total = cosched::n_sets(n_jobs, k);
+  auto boundary = [&](int r) -> int64_t {  // smallest b with C(b,k) >= ceil(r * total / W)
+    if (r <= 0) return 0;
+    if (r >= nranks) return n_jobs;
+    __int128 num = (__int128)r * total;
+    int64_t target = (int64_t)((num + nranks - 1) / nranks);
+    int64_t lo = 0, hi = n_jobs;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (cosched::n_sets(mid, k) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  };
+  int64_t b0 = boundary(rank), b1 = boundary(rank + 1);
+  *first = cosched::n_sets(b0, k);
+  *count = cosched::n_sets(b1, k) - *first;
+}
+
+cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets_out) {
+  if (!h || !first_set || !n_sets_out || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad shard_range arguments");
+  shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, first_set, n_sets_out);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_shard_range_for(int64_t n_jobs, int32_t n_slots, int32_t rank, int32_t nranks,
+                                       int64_t* first_set, int64_t* n_sets_out) {
+  if (!first_set || !n_sets_out || n_jobs < 0 || n_slots < 1 || n_slots > 3 || nranks < 1 || rank < 0 ||
+      rank >= nranks)
+    return COSCHED_E_ARG;
+  shard_bounds(n_jobs, n_slots, rank, nranks, first_set, n_sets_out);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes) {
+  if (!h || !bytes || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad workspace_size arguments");
+  int64_t first, count;
+  shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
+  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, nullptr, nullptr);
+  return COSCHED_OK;
+}
+
+// ---- NCCL ---------------------------------------------------------------------
+cosched_status cosched_get_unique_id(void* uid_out) {
+  std::string why;
+  if (!uid_out) return COSCHED_E_ARG;
+  if (!nccl_load(&why)) {
+    g_create_error = why;
+    return COSCHED_E_NCCL;
+  }
+  ncclUniqueId id;
+  int r = g_nccl.getUniqueId(&id);
+  if (r != 0) return COSCHED_E_NCCL;
+  memcpy(uid_out, &id, sizeof id);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_set_comm(cosched_t h, const void* uid, int rank, int nranks) {
+  if (!h || nranks < 1 || rank < 0 || rank >= nranks) return fail(h, COSCHED_E_ARG, "bad rank/nranks");
+  DeviceGuard g(h->device);
+  if (h->comm) {
+    g_nccl.commDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  h->scored = false;
+  if (nranks == 1) {
+    h->rank = 0;
+    h->nranks = 1;
+    h->view_nranks = 1;
+    return COSCHED_OK;
+  }
+  std::string why;
+  if (!uid) return fail(h, COSCHED_E_ARG, "null unique id");
+  if (!nccl_load(&why)) return fail(h, COSCHED_E_NCCL, why);
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof id);
+  int r = g_nccl.commInitRank(&h->comm, nranks, id, rank);
+  if (r != 0) {
+    h->comm = nullptr;
+    return fail(h, COSCHED_E_NCCL, std::string("ncclCommInitRank: ") +
+                                       (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  }
+  h->rank = rank;
+  h->nranks = nranks;
+  h->view_nranks = 1;
+  return COSCHED_OK;
+}
+
+cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks) {
+  if (!h || nranks < 1 || rank < 0 || rank >= nranks) return fail(h, COSCHED_E_ARG, "bad rank/nranks");
+  if (h->comm) return fail(h, COSCHED_E_STATE, "a communicator is set");
+  h->rank = rank;
+  h->view_nranks = nranks;
+  h->scored = false;
+  return COSCHED_OK;
+}
+
+static cosched_status allreduce_max(cosched_t h, void* dev, size_t count, int dtype) {
+  if (h->nranks <= 1) return COSCHED_OK;
+  int r = g_nccl.allReduce(dev, dev, count, dtype, kNcclMax, h->comm, h->stream);
+  if (r != 0)
+    return fail(h, COSCHED_E_NCCL, std::string("ncclAllReduce: ") +
+                                       (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  return COSCHED_OK;
+}
+
+// ---- scoring --------------------------------------------------------------------
+cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t n_rows, const int32_t* jobs_dev,
+                                 int64_t n_jobs, void* workspace_dev, size_t workspace_bytes, const cosched_out* out,
+                                 void* cuda_stream) {
+  if (!h) return COSCHED_E_ARG;
+  h->err.clear();
+  if (n_jobs < 0 || n_rows < 0 || (n_jobs > 0 && !features_dev) || (!jobs_dev && n_rows < n_jobs))
+    return fail(h, COSCHED_E_ARG, "bad features / jobs arguments");
+  if (cosched::n_sets(n_jobs, h->n_slots) > 0xFFFFFFFEll)
+    return fail(h, COSCHED_E_ARG, "queue too large: more than 2^32-2 sets");
+  int64_t first, count;
+  shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
+  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, nullptr, nullptr);
+  if (!workspace_dev || workspace_bytes < need || ((uintptr_t)workspace_dev & 255))
+    return fail(h, COSCHED_E_OOM, "workspace missing, misaligned or smaller than cosched_workspace_size");
+  float* obj = nullptr;
+  int32_t* cfg = nullptr;
+  if (out) {
+    if (out->first_set != first || out->n_sets != count)
+      return fail(h, COSCHED_E_ARG, "out range differs from cosched_shard_range");
+    obj = out->obj;
+    cfg = out->cfg;
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  Workspace ws;
+  workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, (char*)workspace_dev, &ws);
+  launch_fill_u64(ws.err, ~0ull, 1, st);
+  launch_fill_u64(ws.best_key, 0ull, 1, st);
+  h->launches += 2;
+  if (n_jobs > 0) {
+    launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, st);
+    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, st);
+    h->launches += 2;
+  }
+  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
+  h->scored = true;
+  h->n_jobs = n_jobs;
+  h->first = first;
+  h->n_sets = count;
+  h->ws = ws;
+  h->out_obj = obj;
+  h->out_cfg = cfg;
+  h->stream = st;
+  return COSCHED_OK;
+}
+
+static cosched_status check_deferred(cosched_t h) {
+  CK(cudaMemcpyAsync(h->h_pinned, h->ws.err, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  unsigned long long e = h->h_pinned[0];
+  if (e == ~0ull) return COSCHED_OK;
+  int code = (int)(e & 0xFF);
+  long long pos = (long long)(e >> 8);
+  char buf[160];
+  const char* what = code == COSCHED_E_RANGE ? "counter NaN/outside [0,100] or F6+F7+F8 > 100"
+                     : code == COSCHED_E_DEGENERATE_PROFILE ? "F1 <= 0.01 (degenerate profile)"
+                                                            : "row index outside [0, n_rows)";
+  snprintf(buf, sizeof buf, "job %lld: %s", pos, what);
+  return fail(h, (cosched_status)code, buf);
+}
+
+cosched_status cosched_local_best_key(cosched_t h, uint64_t* key) {
+  if (!h || !key) return fail(h, COSCHED_E_ARG, "null argument");
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  DeviceGuard g(h->device);
+  cosched_status st = check_deferred(h);
+  if (st != COSCHED_OK) return st;
+  CK(cudaMemcpyAsync(h->h_pinned, h->ws.best_key, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  *key = h->h_pinned[0];
+  return COSCHED_OK;
+}
+
+static cosched_status detail_rows(cosched_t h, const int64_t* ids, int64_t n, std::vector<float>* rows) {
+  rows->assign((size_t)n * 8, 0.0f);
+  for (int64_t off = 0; off < n; off += cosched_ctx::kDetailRows) {
+    int64_t m = std::min<int64_t>(cosched_ctx::kDetailRows, n - off);
+    CK(cudaMemcpyAsync(h->d_detail_ids, ids + off, m * 8, cudaMemcpyHostToDevice, h->stream));
+    launch_sets_detail(h->sp, h->ws.ka, h->ws.kb, h->d_detail_ids, m, h->d_detail, h->stream);
+    h->launches++;
+    CK(cudaMemcpyAsync(rows->data() + off * 8, h->d_detail, m * 8 * 4, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return COSCHED_OK;
+}
+
+cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj) {
+  if (!h) return COSCHED_E_ARG;
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  DeviceGuard g(h->device);
+  cosched_status st = check_deferred(h);
+  if (st != COSCHED_OK) return st;
+  st = allreduce_max(h, h->ws.best_key, 1, kNcclUint64);
+  if (st != COSCHED_OK) return st;
+  CK(cudaMemcpyAsync(h->h_pinned, h->ws.best_key, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  uint64_t key = h->h_pinned[0];
+  float o;
+  int64_t sid;
+  cosched_unpack_key(key, &o, &sid);
+  if (set_id) *set_id = sid;
+  if (obj) *obj = o;
+  if (cfg) *cfg = -1;
+  if (key == 0) return COSCHED_INFEASIBLE;
+  if (cfg) {
+    std::vector<float> rows;
+    st = detail_rows(h, &sid, 1, &rows);
+    if (st != COSCHED_OK) return st;
+    int32_t c;
+    memcpy(&c, &rows[0], 4);
+    *cfg = c;
+  }
+  return COSCHED_OK;
+}
+
+cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, float* obj, float* rperf,
+                                   float* throughput, float* fairness) {
+  if (!h) return COSCHED_E_ARG;
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  if (set_id < 0 || set_id >= cosched::n_sets(h->n_jobs, h->n_slots)) return fail(h, COSCHED_E_ARG, "set id out of range");
+  DeviceGuard g(h->device);
+  cosched_status st = check_deferred(h);
+  if (st != COSCHED_OK) return st;
+  std::vector<float> rows;
+  st = detail_rows(h, &set_id, 1, &rows);
+  if (st != COSCHED_OK) return st;
+  int32_t c;
+  memcpy(&c, &rows[0], 4);
+  if (cfg) *cfg = c;
+  if (obj) *obj = rows[1];
+  if (throughput) *throughput = rows[2];
+  if (fairness) *fairness = rows[3];
+  if (rperf)
+    for (int i = 0; i < h->n_slots; i++) rperf[i] = c >= 0 ? rows[4 + i] : NAN;
+  return c >= 0 ? COSCHED_OK : COSCHED_INFEASIBLE;
+}
+
+// ---- allocation -------------------------------------------------------------------
+static int64_t n_partitions(int k, int64_t n) {
+  if (n % k) return 0;
+  int64_t acc = 1;
+  for (int64_t m = n - 1; m > 0; m -= k) acc *= (k == 2) ? m : m * (m - 1) / 2;
+  return acc;
+}
+
+cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids, int32_t* cfgs, double* total_obj,
+                                       int32_t* n_found) {
+  if (!h || k < 1 || !set_ids) return fail(h, COSCHED_E_ARG, "bad allocation arguments");
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  DeviceGuard g(h->device);
+  cosched_status st = check_deferred(h);
+  if (st != COSCHED_OK) return st;
+  const int ns = h->n_slots;
+  const int64_t N = h->n_jobs;
+  if (n_found) *n_found = 0;
+  if (total_obj) *total_obj = 0.0;
+  if (ns < 2) return fail(h, COSCHED_E_ARG, "allocation needs n_slots >= 2");
+  bool exact = (int64_t)k * ns == N && ((ns == 2 && N <= 20) || (ns == 3 && N <= 15));
+  if (exact) {
+    // score every set of the (tiny) queue locally: no collective needed
+    int64_t all = cosched::n_sets(N, ns);
+    launch_fill_u64(h->d_small_key, 0ull, 2, h->stream);
+    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, 0, all, h->d_small_obj, h->d_small_cfg,
+                                    h->d_small_key, h->ws.err, h->variant, h->stream);
+    int64_t nm = n_partitions(ns, N);
+    launch_exact_alloc(ns, N, h->d_small_obj, nm, h->d_small_key + 1, h->stream);
+    launch_exact_unrank(ns, N, h->d_small_key + 1, h->d_small_ids, h->stream);
+    h->launches += 2;
+    std::vector<int64_t> ids(k + 1);
+    std::vector<float> objs(all);
+    std::vector<int32_t> cf(all);
+    CK(cudaMemcpyAsync(ids.data(), h->d_small_ids, (k + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->h_pinned, h->d_small_key + 1, 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(objs.data(), h->d_small_obj, all * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(cf.data(), h->d_small_cfg, all * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    uint64_t key = h->h_pinned[0];
+    if (key == 0) return COSCHED_INFEASIBLE;
+    for (int i = 0; i < k; i++) {
+      set_ids[i] = ids[i];
+      if (cfgs) cfgs[i] = cf[ids[i]];
+    }
+    if (total_obj) *total_obj = (double)unord_float((uint32_t)(key >> 32));
+    if (n_found) *n_found = k;
+    return COSCHED_OK;
+  }
+  // greedy: locally dominant rounds over this rank's shard
+  if (!h->out_obj) return fail(h, COSCHED_E_STATE, "greedy allocation needs score_all with out->obj");
+  Workspace& ws = h->ws;
+  int64_t* cnt = ws.counters;  // [0] n_alive, [1] n_picked, [2] n_alive2
+  launch_fill_u64((unsigned long long*)cnt, 0ull, 8, h->stream);
+  launch_fill_u32(ws.taken, 0u, N, h->stream);
+  launch_greedy_init(ns, N, h->out_obj, h->first, h->n_sets, ws.alive, cnt + 0, h->stream);
+  h->launches += 3;
+  int64_t* alive = ws.alive;
+  int64_t* alive2 = ws.alive2;
+  int64_t host_cnt[8];
+  CK(cudaMemcpyAsync(host_cnt, cnt, 64, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  int64_t n_alive = host_cnt[0], n_picked = 0;
+  for (int round = 0; round < 1000000; round++) {
+    int64_t any_alive = n_alive;
+    if (h->nranks > 1) {
+      // global termination: max over ranks of the alive count
+      CK(cudaMemcpyAsync(cnt + 4, &any_alive, 8, cudaMemcpyHostToDevice, h->stream));
+      st = allreduce_max(h, cnt + 4, 1, kNcclUint64);
+      if (st != COSCHED_OK) return st;
+      CK(cudaMemcpyAsync(&any_alive, cnt + 4, 8, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    if (any_alive == 0) break;
+    launch_fill_u64(ws.job_key, 0ull, N, h->stream);
+    launch_greedy_propose(ns, N, h->out_obj, h->first, alive, n_alive, ws.taken, ws.job_key, h->stream);
+    h->launches += 2;
+    st = allreduce_max(h, ws.job_key, N, kNcclUint64);
+    if (st != COSCHED_OK) return st;
+    launch_greedy_select(ns, N, h->out_obj, h->first, alive, n_alive, ws.job_key, ws.taken, ws.picked, cnt + 1,
+                         h->stream);
+    CK(cudaMemcpyAsync(host_cnt, cnt, 64, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    int64_t now = host_cnt[1];
+    launch_greedy_mark(ns, ws.picked, n_picked, now, ws.taken, h->stream);
+    h->launches += 2;
+    n_picked = now;
+    st = allreduce_max(h, ws.taken, N, kNcclUint32);
+    if (st != COSCHED_OK) return st;
+    launch_fill_u64((unsigned long long*)(cnt + 2), 0ull, 1, h->stream);
+    launch_greedy_compact(ns, N, alive, n_alive, ws.taken, alive2, cnt + 2, h->stream);
+    h->launches += 2;
+    CK(cudaMemcpyAsync(host_cnt, cnt, 64, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    n_alive = host_cnt[2];
+    std::swap(alive, alive2);
+  }
+  // gather picks: per-job key of the set that took it, max over ranks
+  launch_fill_u64(ws.job_key, 0ull, N, h->stream);
+  h->launches++;
+  std::vector<unsigned long long> mine(n_picked);
+  if (n_picked) {
+    CK(cudaMemcpyAsync(mine.data(), ws.picked, n_picked * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  std::vector<unsigned long long> all_keys;
+  if (h->nranks > 1) {
+    // job_key[j] = key of the set containing j (a set's key lands on each of its jobs)
+    std::vector<unsigned long long> jk(N, 0ull);
+    for (unsigned long long key : mine) {
+      int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+      int64_t pos[3];
+      cosched_unrank(N, ns, sid, pos);
+      for (int i = 0; i < ns; i++) jk[pos[i]] = key;
+    }
+    CK(cudaMemcpyAsync(ws.job_key, jk.data(), N * 8, cudaMemcpyHostToDevice, h->stream));
+    st = allreduce_max(h, ws.job_key, N, kNcclUint64);
+    if (st != COSCHED_OK) return st;
+    CK(cudaMemcpyAsync(jk.data(), ws.job_key, N * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int64_t j = 0; j < N; j++)
+      if (jk[j]) all_keys.push_back(jk[j]);
+    std::sort(all_keys.begin(), all_keys.end());
+    all_keys.erase(std::unique(all_keys.begin(), all_keys.end()), all_keys.end());
+    CK(cudaMemcpyAsync(ws.picked, all_keys.data(), all_keys.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    n_picked = (int64_t)all_keys.size();
+  }
+  if (n_picked == 0) return COSCHED_INFEASIBLE;
+  // order picks by key, descending = sequential greedy order (on the GPU)
+  unsigned long long* sorted = ws.job_key;  // reuse: n_picked <= N / n_slots
+  launch_sort_keys_desc(ws.picked, n_picked, sorted, h->stream);
+  h->launches++;
+  int64_t take = std::min<int64_t>(k, n_picked);
+  std::vector<unsigned long long> top(take);
+  CK(cudaMemcpyAsync(top.data(), sorted, take * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  std::vector<int64_t> ids(take);
+  double tot = 0.0;
+  for (int64_t i = 0; i < take; i++) {
+    float o;
+    cosched_unpack_key(top[i], &o, &ids[i]);
+    set_ids[i] = ids[i];
+    tot += (double)o;
+  }
+  if (cfgs) {
+    std::vector<float> rows;
+    st = detail_rows(h, ids.data(), take, &rows);
+    if (st != COSCHED_OK) return st;
+    for (int64_t i = 0; i < take; i++) memcpy(&cfgs[i], &rows[i * 8], 4);
+  }
+  if (total_obj) *total_obj = tot;
+  if (n_found) *n_found = (int32_t)take;
+  return COSCHED_OK;
+}
+
+}  // extern "C"

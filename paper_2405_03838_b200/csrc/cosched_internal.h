@@ -1,0 +1,102 @@
+// cosched_internal.h -- shared declarations of the CUDA path (kernels + C-ABI host code).
+// Nothing here is shared with oracle/ (the test oracle); see DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cosched.h"
+
+namespace cosched {
+
+constexpr int kMaxCaps = 64;
+constexpr int kMaxStates = 128;
+constexpr int kMaxSlices = 128;
+constexpr int kMaxSlots = 3;
+
+// Feasibility scale: the projection stores
+// K*(U - alpha) and K*V, so a slot's margin r - alpha appears as
+// r'' = K*(r - alpha), exactly (K is a power of two), and the masked objective
+// min3(obj, r0'', r1'') equals obj unless a margin is below obj/K (< 1e-11).
+constexpr float kScale = 1099511627776.0f;  // 2^40
+constexpr float kInvScale = 1.0f / 1099511627776.0f;
+
+// Everything a scoring kernel needs about the search space, passed by value
+// (kernel parameter space -> constant bank, read with c[0x0][...] operands).
+struct SpaceParams {
+  int32_t n_slots;
+  int32_t n_states;
+  int32_t n_slices;
+  int32_t n_caps;
+  int32_t np;                 // caps padded to a multiple of 4 (row length of the projection)
+  int32_t n_cfg;              // n_states * n_caps
+  float alpha;
+  float obj_scale[kMaxCaps];  // per cap: invP/K (Problem 2) or 1/K (Problem 1)
+  float obj_bias[kMaxCaps];   // per cap: n_slots*alpha*invP (Problem 2) or n_slots*alpha (Problem 1)
+  int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
+};
+
+// Device-side tables owned by a handle.
+struct DeviceTables {
+  float* coef_c = nullptr;  // [n_caps][n_slices][6]
+  float* coef_d = nullptr;  // [n_caps][n_slices][3]
+};
+
+// Workspace layout (carved from the caller's buffer, all 256-byte aligned).
+struct Workspace {
+  float* ka = nullptr;              // [n_jobs][n_slices][np] = K*(U - alpha); padding = -1e30
+  float* kb = nullptr;              // [n_jobs][n_slices][np] = K*V;           padding = -1e30
+  unsigned long long* best_key = nullptr;  // [1] shard argmax key
+  unsigned long long* err = nullptr;       // [1] first bad job: (pos << 8) | status, ~0 = none
+  unsigned long long* job_key = nullptr;   // [n_jobs] greedy per-job best keys
+  uint32_t* taken = nullptr;               // [n_jobs] greedy taken marks
+  int64_t* alive = nullptr;                // [n_sets_local] greedy alive list
+  int64_t* alive2 = nullptr;               // [n_sets_local]
+  unsigned long long* picked = nullptr;    // [n_jobs] greedy picked keys
+  int64_t* counters = nullptr;             // [8] device counters
+  size_t bytes = 0;
+};
+
+size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t np, int64_t n_sets_local, char* base,
+                        Workspace* ws);
+
+// ---- kernel launchers (defined in kernels.cu) ------------------------------------
+void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
+                     unsigned long long* err, cudaStream_t st);
+void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
+                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, cudaStream_t st);
+// Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
+// maxes the packed key into *best_key. Returns the number of kernels launched.
+int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb,
+                 int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                 const unsigned long long* err, int variant, cudaStream_t st);
+void launch_exact_alloc(int n_slots, int64_t n_jobs, const float* set_obj, int64_t n_match,
+                        unsigned long long* best_key, cudaStream_t st);
+void launch_exact_unrank(int n_slots, int64_t n_jobs, const unsigned long long* best_key, int64_t* set_ids,
+                         cudaStream_t st);
+// greedy (locally dominant rounds)
+void launch_greedy_init(int n_slots, int64_t n_jobs, const float* obj, int64_t first, int64_t count,
+                        int64_t* alive, int64_t* n_alive, cudaStream_t st);
+void launch_greedy_propose(int n_slots, int64_t n_jobs, const float* obj, int64_t first, const int64_t* alive,
+                           int64_t n_alive, const uint32_t* taken, unsigned long long* job_key, cudaStream_t st);
+void launch_greedy_select(int n_slots, int64_t n_jobs, const float* obj, int64_t first, const int64_t* alive,
+                          int64_t n_alive, const unsigned long long* job_key, uint32_t* taken,
+                          unsigned long long* picked, int64_t* n_picked, cudaStream_t st);
+void launch_greedy_mark(int n_slots, const unsigned long long* picked, int64_t from, int64_t to, uint32_t* taken,
+                        cudaStream_t st);
+void launch_sort_keys_desc(const unsigned long long* keys, int64_t n, unsigned long long* sorted, cudaStream_t st);
+void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const int64_t* set_ids, int64_t n,
+                        float* out /* [n][4 + kMaxSlots] */, cudaStream_t st);
+void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive,
+                           const uint32_t* taken, int64_t* alive_out, int64_t* n_out, cudaStream_t st);
+void launch_fill_u64(unsigned long long* p, unsigned long long v, int64_t n, cudaStream_t st);
+void launch_fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t st);
+
+// host-side helpers shared by the API (no CUDA)
+int64_t n_sets(int64_t n, int k);
+uint32_t ord_float(float f);
+float unord_float(uint32_t o);
+
+}  // namespace cosched

@@ -1,0 +1,89 @@
+// device_common.cuh -- small device helpers of the CUDA path.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace cosched {
+
+// Table `functions` in FP32, IEEE division (no fast-math):
+//   H = (F1/100 - H2, (F6+F7+F8)/100, F2/F1, F4/100, F5/100, 1),  J = (F3/100, F4/100, 1)
+__device__ __forceinline__ void basis_hj(const float* __restrict__ f, float h[6], float j[3]) {
+  float f1 = f[0], f2 = f[1], f3 = f[2], f4 = f[3], f5 = f[4];
+  float tensor = __fadd_rn(__fadd_rn(f[5], f[6]), f[7]);
+  h[1] = __fdiv_rn(tensor, 100.0f);
+  h[0] = __fsub_rn(__fdiv_rn(f1, 100.0f), h[1]);
+  h[2] = __fdiv_rn(f2, f1);
+  h[3] = __fdiv_rn(f4, 100.0f);
+  h[4] = __fdiv_rn(f5, 100.0f);
+  h[5] = 1.0f;
+  j[0] = __fdiv_rn(f3, 100.0f);
+  j[1] = __fdiv_rn(f4, 100.0f);
+  j[2] = 1.0f;
+}
+
+// order-preserving float -> u32 (larger float <=> larger u32; -0 < +0)
+__device__ __forceinline__ uint32_t ord_float_d(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Packed argmax key: larger objective first, then lower set id. Unique per set.
+__device__ __forceinline__ unsigned long long pack_key(float obj, int64_t sid) {
+  return ((unsigned long long)ord_float_d(obj) << 32) | (0xFFFFFFFFull - (unsigned long long)(uint32_t)sid);
+}
+
+__device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
+__device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
+
+// colex unranking: set id -> ascending queue positions
+template <int NS>
+__device__ __forceinline__ void unrank_set(int64_t id, int64_t* j) {
+  if (NS == 1) {
+    j[0] = id;
+  } else if (NS == 2) {
+    int64_t b = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)id)) * 0.5);
+    while (c2(b) > id) b--;
+    while (c2(b + 1) <= id) b++;
+    j[1] = b;
+    j[0] = id - c2(b);
+  } else {
+    int64_t c = (int64_t)cbrt(6.0 * (double)id) + 1;
+    while (c3(c) > id) c--;
+    while (c3(c + 1) <= id) c++;
+    int64_t rest = id - c3(c);
+    int64_t b = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)rest)) * 0.5);
+    while (c2(b) > rest) b--;
+    while (c2(b + 1) <= rest) b++;
+    j[2] = c;
+    j[1] = b;
+    j[0] = rest - c2(b);
+  }
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Block-wide max of a per-thread key, then one atomicMax per block. The max of
+// unique keys does not depend on the order, so the result is deterministic.
+__device__ __forceinline__ void block_max_key(unsigned long long key, unsigned long long* dst) {
+  __shared__ unsigned long long s_part[32];
+  key = warp_max_u64(key);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_part[w] = key;
+  __syncthreads();
+  if (w == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    unsigned long long v = lane < nw ? s_part[lane] : 0ull;
+    v = warp_max_u64(v);
+    if (lane == 0 && v) atomicMax(dst, v);
+  }
+}
+
+}  // namespace cosched

@@ -1,0 +1,522 @@
+// kernels.cu -- the CUDA path of the co-location search (sm_100a).
+//
+// Steps: a1 validate features, a2 basis H/J,
+// a3 projection onto C/D (the exact factorisation of P:L458), a4-a7 set
+// enumeration + model evaluation + objective/fairness + per-set argmax,
+// a8 per-shard argmax key, a10 allocation (exact / greedy).
+//
+// The fast pair scorer lives in score_pairs.cu; this file holds the generic
+// scorer (any n_slots, also the reference for the fast one), the per-set
+// detail evaluator and the allocation kernels.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "cosched_internal.h"
+#include "device_common.cuh"
+
+namespace cosched {
+
+// ---------------------------------------------------------------------------
+// a1: validation (SPEC.md L26-27 ranges, L54/L87 degenerate F1). One thread per
+// queue position; the first bad position wins through an atomicMin on
+// (pos << 8 | status).
+__global__ void k_validate(const float* __restrict__ F, int64_t n_rows, const int32_t* __restrict__ jobs,
+                           int64_t n_jobs, unsigned long long* err) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_jobs) return;
+  int64_t row = jobs ? (int64_t)jobs[q] : q;
+  int code = 0;
+  if (row < 0 || row >= n_rows) {
+    code = COSCHED_E_ARG;
+  } else {
+    const float* f = F + row * 8;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = f[k];
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      if (!(v[k] >= 0.0f && v[k] <= 100.0f)) code = COSCHED_E_RANGE;
+    if (!code) {
+      float tensor = __fadd_rn(__fadd_rn(v[5], v[6]), v[7]);
+      if (!(tensor <= 100.0f)) code = COSCHED_E_RANGE;
+      else if (!(v[0] > 0.01f)) code = COSCHED_E_DEGENERATE_PROFILE;
+    }
+  }
+  if (code) atomicMin(err, ((unsigned long long)q << 8) | (unsigned long long)code);
+}
+
+void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
+                     unsigned long long* err, cudaStream_t st) {
+  if (n_jobs <= 0) return;
+  int bs = 256;
+  k_validate<<<(unsigned)((n_jobs + bs - 1) / bs), bs, 0, st>>>(features, n_rows, jobs, n_jobs, err);
+}
+
+// ---------------------------------------------------------------------------
+// a2 + a3: basis and projection. Thread per (job, slice, padded cap):
+//   U = C[p][s] . H(F_n),  V = D[p][s] . J(F_n)   (the two dot products of P:L458)
+//   ka = K*(U - alpha),   kb = K*V               (exact power-of-two scaling)
+// Padding caps (p >= n_caps) get -1e30 so every candidate using them is infeasible.
+__global__ void k_project(const float* __restrict__ F, const int32_t* __restrict__ jobs, int64_t n_jobs,
+                          const SpaceParams sp, const float* __restrict__ coef_c,
+                          const float* __restrict__ coef_d, const unsigned long long* __restrict__ err,
+                          float* __restrict__ ka, float* __restrict__ kb) {
+  if (*err != ~0ull) return;  // invalid input: leave the workspace untouched
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = n_jobs * sp.n_slices * sp.np;
+  if (idx >= total) return;
+  int p = (int)(idx % sp.np);
+  int64_t ns = idx / sp.np;
+  int s = (int)(ns % sp.n_slices);
+  int64_t n = ns / sp.n_slices;
+  if (p >= sp.n_caps) {
+    ka[idx] = -1e30f;
+    kb[idx] = -1e30f;
+    return;
+  }
+  int64_t row = jobs ? (int64_t)jobs[n] : n;
+  float h[6], j[3];
+  basis_hj(F + row * 8, h, j);
+  const float* C = coef_c + ((int64_t)p * sp.n_slices + s) * 6;
+  const float* D = coef_d + ((int64_t)p * sp.n_slices + s) * 3;
+  float u = __fmul_rn(C[0], h[0]);
+#pragma unroll
+  for (int t = 1; t < 6; t++) u = __fmaf_rn(C[t], h[t], u);
+  float v = __fmul_rn(D[0], j[0]);
+#pragma unroll
+  for (int t = 1; t < 3; t++) v = __fmaf_rn(D[t], j[t], v);
+  ka[idx] = __fmul_rn(__fsub_rn(u, sp.alpha), kScale);
+  kb[idx] = __fmul_rn(v, kScale);
+}
+
+void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
+                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb,
+                    cudaStream_t st) {
+  int64_t total = n_jobs * sp.n_slices * sp.np;
+  if (total <= 0) return;
+  int bs = 256;
+  k_project<<<(unsigned)((total + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
+                                                               err, ka, kb);
+}
+
+// ---------------------------------------------------------------------------
+// a4-a8, generic reference scorer: one thread per set. For each config in
+// canonical order (state in table order, caps ascending):
+//   r_i'' = ka[j_i][s_i][p] + sum_{l != i} kb[j_l][s_i][p]   (= K*(RPerf_i - alpha))
+//   t     = sum_i r_i''
+//   obj   = fma(t, obj_scale[p], obj_bias[p])                (= Throughput [/ P])
+//   feasible iff every r_i'' > 0  (Fairness > alpha)
+// keep the first strictly greater feasible obj.
+template <int NS>
+__global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int64_t n_jobs,
+                                                       const float* __restrict__ ka, const float* __restrict__ kb,
+                                                       int64_t first, int64_t count, float* __restrict__ out_obj,
+                                                       int32_t* __restrict__ out_cfg,
+                                                       unsigned long long* __restrict__ best_key,
+                                                       const unsigned long long* __restrict__ err) {
+  if (*err != ~0ull) return;
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long key = 0;
+  if (k < count) {
+    int64_t sid = first + k;
+    int64_t j[3];
+    unrank_set<NS>(sid, j);
+    const int64_t row = (int64_t)sp.n_slices * sp.np;
+    float best = -INFINITY;
+    int32_t bc = -1;
+    for (int s = 0; s < sp.n_states; s++) {
+      const float* a[NS];
+      const float* b[NS][NS];
+#pragma unroll
+      for (int i = 0; i < NS; i++) {
+        int sl = sp.slice[s][i];
+        a[i] = ka + j[i] * row + (int64_t)sl * sp.np;
+#pragma unroll
+        for (int l = 0; l < NS; l++) b[i][l] = kb + j[l] * row + (int64_t)sl * sp.np;
+      }
+      for (int p = 0; p < sp.n_caps; p++) {
+        float t = 0.0f;
+        bool feas = true;
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+          float r = a[i][p];
+#pragma unroll
+          for (int l = 0; l < NS; l++)
+            if (l != i) r = __fadd_rn(r, b[i][l][p]);
+          feas = feas && (r > 0.0f);
+          t = (i == 0) ? r : __fadd_rn(t, r);
+        }
+        float u = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
+        if (feas && u > best) {
+          best = u;
+          bc = s * sp.n_caps + p;
+        }
+      }
+    }
+    if (out_obj) out_obj[k] = bc >= 0 ? best : -INFINITY;
+    if (out_cfg) out_cfg[k] = bc;
+    key = bc >= 0 ? pack_key(best, sid) : 0ull;
+  }
+  block_max_key(key, best_key);
+}
+
+int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, int64_t first,
+                            int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                            const unsigned long long* err, cudaStream_t st);
+
+int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, int64_t first,
+                 int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                 const unsigned long long* err, int variant, cudaStream_t st) {
+  if (count <= 0) return 0;
+  if (variant != 0 && sp.n_slots == 2)
+    return launch_score_pairs_fast(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err, st);
+  int bs = 256;
+  unsigned grid = (unsigned)((count + bs - 1) / bs);
+  if (sp.n_slots == 1)
+    k_score_generic<1><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+  else if (sp.n_slots == 2)
+    k_score_generic<2><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+  else
+    k_score_generic<3><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// Per-set detail (cosched_best_config, winners of best_set / allocation): one
+// block per listed set evaluates every config of it, reduces (obj desc, cfg asc)
+// and reports the winner's RPerf, Throughput, Fairness in natural units
+// (RPerf_i = r_i''/K + alpha).
+// out row (8 floats): [0] cfg (int bits, -1 none), [1] obj, [2] thr, [3] fair, [4..] rperf
+__global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
+                              const int64_t* __restrict__ set_ids, float* out_all) {
+  __shared__ unsigned long long s_key[32];
+  const int64_t set_id = set_ids[blockIdx.x];
+  float* out = out_all + (int64_t)blockIdx.x * 8;
+  int64_t j[3];
+  if (sp.n_slots == 1) unrank_set<1>(set_id, j);
+  else if (sp.n_slots == 2) unrank_set<2>(set_id, j);
+  else unrank_set<3>(set_id, j);
+  const int64_t row = (int64_t)sp.n_slices * sp.np;
+  unsigned long long key = 0;
+  for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
+    int s = c / sp.n_caps, p = c % sp.n_caps;
+    float t = 0.0f;
+    bool feas = true;
+    for (int i = 0; i < sp.n_slots; i++) {
+      int sl = sp.slice[s][i];
+      float r = ka[j[i] * row + (int64_t)sl * sp.np + p];
+      for (int l = 0; l < sp.n_slots; l++)
+        if (l != i) r = __fadd_rn(r, kb[j[l] * row + (int64_t)sl * sp.np + p]);
+      feas = feas && (r > 0.0f);
+      t = (i == 0) ? r : __fadd_rn(t, r);
+    }
+    float u = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
+    unsigned long long kk = feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
+    key = kk > key ? kk : key;
+  }
+  key = warp_max_u64(key);
+  if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = 0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; w++) m = s_key[w] > m ? s_key[w] : m;
+    if (m == 0) {
+      out[0] = __int_as_float(-1);
+      out[1] = -INFINITY;
+      out[2] = out[3] = 0.0f;
+      return;
+    }
+    int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
+    int s = c / sp.n_caps, p = c % sp.n_caps;
+    float thr = 0.0f, fair = INFINITY, t = 0.0f;
+    for (int i = 0; i < sp.n_slots; i++) {
+      int sl = sp.slice[s][i];
+      float r = ka[j[i] * row + (int64_t)sl * sp.np + p];
+      for (int l = 0; l < sp.n_slots; l++)
+        if (l != i) r = __fadd_rn(r, kb[j[l] * row + (int64_t)sl * sp.np + p]);
+      t = (i == 0) ? r : __fadd_rn(t, r);
+      float rp = __fmaf_rn(r, kInvScale, sp.alpha);
+      out[4 + i] = rp;
+      thr = (i == 0) ? rp : __fadd_rn(thr, rp);
+      fair = fminf(fair, rp);
+    }
+    out[0] = __int_as_float(c);
+    out[1] = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
+    out[2] = thr;
+    out[3] = fair;
+  }
+}
+
+void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const int64_t* set_ids, int64_t n,
+                        float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, set_ids, out);
+}
+
+// Rank sort of a short list of unique keys, descending: position of key i =
+// number of keys greater than it (the greedy picks, <= n_jobs / n_slots).
+__global__ void k_sort_keys_desc(const unsigned long long* __restrict__ keys, int64_t n,
+                                 unsigned long long* __restrict__ sorted) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long k = keys[i];
+  int64_t pos = 0;
+  for (int64_t t = 0; t < n; t++) pos += keys[t] > k;
+  sorted[pos] = k;
+}
+
+void launch_sort_keys_desc(const unsigned long long* keys, int64_t n, unsigned long long* sorted, cudaStream_t st) {
+  if (n <= 0) return;
+  k_sort_keys_desc<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(keys, n, sorted);
+}
+
+// ---------------------------------------------------------------------------
+// a10 exact allocation: one thread per partition rank. Rank digits, most
+// significant first: level i picks the d_i-th partner (pairs) or partner pair
+// (triples, lexicographic) among the free jobs above the lowest free job --
+// the enumeration order of DESIGN.md R12. W = sum of per-set objectives in
+// formation order (FP32); partitions with an infeasible set are skipped.
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
+  for (int i = 0; i < n; i++) m &= m - 1;
+  return __ffs(m) - 1;
+}
+
+__device__ bool decode_partition(int n_slots, int n_jobs, int64_t rank, int64_t* ids) {
+  int k = n_jobs / n_slots;
+  // place values
+  int64_t place[16];
+  int64_t acc = 1;
+  for (int i = k - 1; i >= 0; i--) {
+    place[i] = acc;
+    int m = n_jobs - 1 - n_slots * i;
+    int64_t radix = n_slots == 2 ? m : (int64_t)m * (m - 1) / 2;
+    acc *= radix;
+  }
+  if (rank >= acc) return false;
+  uint32_t freem = (n_jobs >= 32) ? 0xFFFFFFFFu : ((1u << n_jobs) - 1u);
+  for (int i = 0; i < k; i++) {
+    int m = n_jobs - 1 - n_slots * i;
+    int64_t radix = n_slots == 2 ? m : (int64_t)m * (m - 1) / 2;
+    int64_t d = (rank / place[i]) % radix;
+    int a = __ffs(freem) - 1;
+    freem &= ~(1u << a);
+    if (n_slots == 2) {
+      int b = nth_set_bit(freem, (int)d);
+      freem &= ~(1u << b);
+      ids[i] = (int64_t)b * (b - 1) / 2 + a;
+    } else {
+      int x = 0;
+      int64_t dd = d;
+      while (dd >= m - 1 - x) {
+        dd -= m - 1 - x;
+        x++;
+      }
+      int y = x + 1 + (int)dd;
+      int b = nth_set_bit(freem, x), c = nth_set_bit(freem, y);
+      freem &= ~(1u << b);
+      freem &= ~(1u << c);
+      ids[i] = (int64_t)c * (c - 1) * (c - 2) / 6 + (int64_t)b * (b - 1) / 2 + a;
+    }
+  }
+  return true;
+}
+
+__global__ void k_exact_alloc(int n_slots, int n_jobs, const float* __restrict__ set_obj, int64_t n_match,
+                              unsigned long long* best_key) {
+  unsigned long long key = 0;
+  int64_t ids[16];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_match;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (!decode_partition(n_slots, n_jobs, r, ids)) continue;
+    int k = n_jobs / n_slots;
+    float w = 0.0f;
+    bool ok = true;
+    for (int i = 0; i < k; i++) {
+      float o = set_obj[ids[i]];
+      ok = ok && (o > -INFINITY);
+      w = (i == 0) ? o : __fadd_rn(w, o);
+    }
+    if (ok) {
+      unsigned long long kk = ((unsigned long long)ord_float_d(w) << 32) | (0xFFFFFFFFull - (uint64_t)r);
+      key = kk > key ? kk : key;
+    }
+  }
+  block_max_key(key, best_key);
+}
+
+void launch_exact_alloc(int n_slots, int64_t n_jobs, const float* set_obj, int64_t n_match,
+                        unsigned long long* best_key, cudaStream_t st) {
+  int bs = 256;
+  int64_t blocks = (n_match + bs - 1) / bs;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_exact_alloc<<<(unsigned)blocks, bs, 0, st>>>(n_slots, (int)n_jobs, set_obj, n_match, best_key);
+}
+
+__global__ void k_exact_unrank(int n_slots, int n_jobs, const unsigned long long* best_key, int64_t* set_ids) {
+  unsigned long long key = *best_key;
+  int k = n_jobs / n_slots;
+  if (key == 0) {
+    for (int i = 0; i < k; i++) set_ids[i] = -1;
+    set_ids[k] = -1;
+    return;
+  }
+  int64_t rank = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+  decode_partition(n_slots, n_jobs, rank, set_ids);
+  set_ids[k] = rank;
+}
+
+void launch_exact_unrank(int n_slots, int64_t n_jobs, const unsigned long long* best_key, int64_t* set_ids,
+                         cudaStream_t st) {
+  k_exact_unrank<<<1, 1, 0, st>>>(n_slots, (int)n_jobs, best_key, set_ids);
+}
+
+// ---------------------------------------------------------------------------
+// a10 greedy allocation as locally-dominant rounds. With unique keys
+// (obj, -set_id), a set that is the best remaining set of every one of its
+// jobs is taken by the sequential greedy too, so iterating
+//   propose: job_key[j] = max key over alive sets with all jobs free
+//   select:  take every alive set whose key equals job_key of all its jobs
+// until nothing is taken reproduces the sequential greedy's full pick set.
+__global__ void k_greedy_init(int n_slots, const float* __restrict__ obj, int64_t first, int64_t count,
+                              int64_t* alive, int64_t* n_alive) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  if (obj[k] > -INFINITY) {
+    int64_t at = (int64_t)atomicAdd((unsigned long long*)n_alive, 1ull);
+    alive[at] = first + k;
+  }
+}
+
+void launch_greedy_init(int n_slots, int64_t n_jobs, const float* obj, int64_t first, int64_t count, int64_t* alive,
+                        int64_t* n_alive, cudaStream_t st) {
+  (void)n_jobs;
+  if (count <= 0) return;
+  k_greedy_init<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(n_slots, obj, first, count, alive, n_alive);
+}
+
+template <int NS>
+__device__ __forceinline__ bool all_free(int64_t sid, const uint32_t* taken, int64_t* j) {
+  unrank_set<NS>(sid, j);
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) ok = ok && (taken[j[i]] == 0);
+  return ok;
+}
+
+template <int NS>
+__global__ void k_greedy_propose(const float* __restrict__ obj, int64_t first, const int64_t* __restrict__ alive,
+                                 int64_t n_alive, const uint32_t* __restrict__ taken,
+                                 unsigned long long* job_key) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_alive) return;
+  int64_t sid = alive[k];
+  int64_t j[3];
+  if (!all_free<NS>(sid, taken, j)) return;
+  unsigned long long key = pack_key(obj[sid - first], sid);
+#pragma unroll
+  for (int i = 0; i < NS; i++)
+    if (job_key[j[i]] < key) atomicMax(&job_key[j[i]], key);
+}
+
+template <int NS>
+__global__ void k_greedy_select(const float* __restrict__ obj, int64_t first, const int64_t* __restrict__ alive,
+                                int64_t n_alive, const unsigned long long* __restrict__ job_key, uint32_t* taken,
+                                unsigned long long* picked, int64_t* n_picked) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_alive) return;
+  int64_t sid = alive[k];
+  int64_t j[3];
+  if (!all_free<NS>(sid, taken, j)) return;
+  unsigned long long key = pack_key(obj[sid - first], sid);
+  bool win = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) win = win && (job_key[j[i]] == key);
+  if (!win) return;
+  int64_t at = (int64_t)atomicAdd((unsigned long long*)n_picked, 1ull);
+  picked[at] = key;
+}
+
+// Marks are applied in a separate pass so that `select` reads a consistent taken[].
+template <int NS>
+__global__ void k_greedy_mark(const unsigned long long* __restrict__ picked, int64_t from, int64_t to,
+                              uint32_t* taken) {
+  int64_t k = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= to) return;
+  int64_t sid = (int64_t)(0xFFFFFFFFull - (picked[k] & 0xFFFFFFFFull));
+  int64_t j[3];
+  unrank_set<NS>(sid, j);
+#pragma unroll
+  for (int i = 0; i < NS; i++) taken[j[i]] = 1;
+}
+
+void launch_greedy_propose(int n_slots, int64_t n_jobs, const float* obj, int64_t first, const int64_t* alive,
+                           int64_t n_alive, const uint32_t* taken, unsigned long long* job_key, cudaStream_t st) {
+  (void)n_jobs;
+  if (n_alive <= 0) return;
+  unsigned g = (unsigned)((n_alive + 255) / 256);
+  if (n_slots == 1) k_greedy_propose<1><<<g, 256, 0, st>>>(obj, first, alive, n_alive, taken, job_key);
+  else if (n_slots == 2) k_greedy_propose<2><<<g, 256, 0, st>>>(obj, first, alive, n_alive, taken, job_key);
+  else k_greedy_propose<3><<<g, 256, 0, st>>>(obj, first, alive, n_alive, taken, job_key);
+}
+
+void launch_greedy_select(int n_slots, int64_t n_jobs, const float* obj, int64_t first, const int64_t* alive,
+                          int64_t n_alive, const unsigned long long* job_key, uint32_t* taken,
+                          unsigned long long* picked, int64_t* n_picked, cudaStream_t st) {
+  (void)n_jobs;
+  if (n_alive <= 0) return;
+  unsigned g = (unsigned)((n_alive + 255) / 256);
+  if (n_slots == 1) k_greedy_select<1><<<g, 256, 0, st>>>(obj, first, alive, n_alive, job_key, taken, picked, n_picked);
+  else if (n_slots == 2) k_greedy_select<2><<<g, 256, 0, st>>>(obj, first, alive, n_alive, job_key, taken, picked, n_picked);
+  else k_greedy_select<3><<<g, 256, 0, st>>>(obj, first, alive, n_alive, job_key, taken, picked, n_picked);
+}
+
+void launch_greedy_mark(int n_slots, const unsigned long long* picked, int64_t from, int64_t to, uint32_t* taken,
+                        cudaStream_t st) {
+  if (to <= from) return;
+  unsigned g = (unsigned)((to - from + 255) / 256);
+  if (n_slots == 1) k_greedy_mark<1><<<g, 256, 0, st>>>(picked, from, to, taken);
+  else if (n_slots == 2) k_greedy_mark<2><<<g, 256, 0, st>>>(picked, from, to, taken);
+  else k_greedy_mark<3><<<g, 256, 0, st>>>(picked, from, to, taken);
+}
+
+template <int NS>
+__global__ void k_greedy_compact(const int64_t* __restrict__ alive, int64_t n_alive, const uint32_t* __restrict__ taken,
+                                 int64_t* alive_out, int64_t* n_out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_alive) return;
+  int64_t sid = alive[k];
+  int64_t j[3];
+  if (!all_free<NS>(sid, taken, j)) return;
+  int64_t at = (int64_t)atomicAdd((unsigned long long*)n_out, 1ull);
+  alive_out[at] = sid;
+}
+
+void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive, const uint32_t* taken,
+                           int64_t* alive_out, int64_t* n_out, cudaStream_t st) {
+  (void)n_jobs;
+  if (n_alive <= 0) return;
+  unsigned g = (unsigned)((n_alive + 255) / 256);
+  if (n_slots == 1) k_greedy_compact<1><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
+  else if (n_slots == 2) k_greedy_compact<2><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
+  else k_greedy_compact<3><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_fill_u64(unsigned long long* p, unsigned long long v, int64_t n) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) p[k] = v;
+}
+__global__ void k_fill_u32(uint32_t* p, uint32_t v, int64_t n) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) p[k] = v;
+}
+void launch_fill_u64(unsigned long long* p, unsigned long long v, int64_t n, cudaStream_t st) {
+  if (n > 0) k_fill_u64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, v, n);
+}
+void launch_fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t st) {
+  if (n > 0) k_fill_u32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, v, n);
+}
+
+}  // namespace cosched

@@ -1,0 +1,279 @@
+"""GPU (CUDA path through the C-ABI) vs the FP64 oracle, on seeded synthetic inputs.
+
+Bar: chosen config / set / allocation indices equal to the oracle's up to the
+tie-aware rule of tests/parity.py (objectives within 1e-5 relative); integer
+outputs (set ids, unranking, counts, statuses) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import Oracle  # noqa: E402
+from synth import bench_config, make_features, make_problem, tie_stress_features  # noqa: E402
+from parity import TAU_OBJ, accept_set, check_sets, replay_greedy  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_03838_b200 as cs
+    return cs
+
+
+def _run(cs, pb, F, jobs=None, variant=None):
+    s = cs.Scheduler(pb)
+    if variant is not None:
+        s.set_variant(variant)
+    Fd = torch.from_numpy(np.ascontiguousarray(F)).cuda()
+    Jd = None if jobs is None else torch.from_numpy(np.ascontiguousarray(jobs, dtype=np.int32)).cuda()
+    obj, cfg = s.score_all(Fd, Jd)
+    torch.cuda.synchronize()
+    return s, obj.cpu().numpy(), cfg.cpu().numpy()
+
+
+def _full_parity(cs, pb, F, jobs=None, variant=None):
+    s, obj_g, cfg_g = _run(cs, pb, F, jobs, variant)
+    n = F.shape[0] if jobs is None else len(jobs)
+    o = Oracle(pb)
+    cfg_o, obj_o = o.score_range(F, jobs)
+    assert len(cfg_g) == len(cfg_o)
+    mism = np.nonzero(cfg_g != cfg_o)[0]
+    # where the index agrees the objective must agree to 1e-5 relative
+    same = (cfg_g == cfg_o) & (cfg_o >= 0)
+    rel = np.abs(obj_g[same].astype(np.float64) - obj_o[same]) / np.abs(obj_o[same])
+    assert rel.max(initial=0) <= TAU_OBJ, rel.max()
+    assert np.all(obj_g[cfg_g < 0] == -np.inf)
+    # index disagreements must be ties under the tie-aware rule
+    exact, fails = check_sets(o, F, jobs, mism, cfg_g[mism], obj_g[mism], n, pb.n_slots)
+    assert not fails, fails[:5]
+    return s, obj_g, cfg_g, cfg_o, obj_o, len(mism)
+
+
+# ---- configs C1-C3 exhaustively ------------------------------------------------
+
+def test_c1_single_pair(cs):
+    pb, F = bench_config("C1")
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F)
+    assert nm == 0 and cfg_g[0] == cfg_o[0]
+    d = s.best_config(0)
+    o = Oracle(pb)
+    _, fair, thr, _, rp = o.eval_set([F[0], F[1]])
+    c = d["cfg"]
+    assert np.allclose(d["rperf"], rp[c], atol=1e-5) and abs(d["throughput"] - thr[c]) < 1e-5
+    assert abs(d["fairness"] - fair[c]) < 1e-5
+    st, sid, cfg, ob = s.best_set()
+    assert (st, sid, cfg) == (0, 0, cfg_o[0])
+
+
+def test_c2_pairs_best_set_and_exact_allocation(cs):
+    pb, F = bench_config("C2")
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F)
+    st, sid, cfg, ob = s.best_set()
+    ost, osid, ocfg, oob = Oracle(pb).best_set(F)
+    assert st == ost == 0
+    assert sid == osid or obj_o[sid] >= oob * (1 - TAU_OBJ)
+    # exact allocation over the 105 pairings (BASELINE.json config 2)
+    st, ids, cfgs, tot = s.best_allocation(4)
+    ost, rank, oids, otot, nmatch = oracle.exact_allocation(8, 2, obj_o)
+    assert nmatch == 105 and st == ost == 0
+    w_gpu_by_oracle = sum(obj_o[i] for i in ids)
+    assert ids == oids or w_gpu_by_oracle >= otot * (1 - TAU_OBJ)
+    assert abs(tot - otot) <= TAU_OBJ * abs(otot)
+    assert sorted(sum((list(oracle.unrank(8, 2, i)) for i in ids), [])) == list(range(8))
+    assert cfgs == [int(cfg_g[i]) for i in ids]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c3_all_pairs(cs, variant):
+    pb, F = bench_config("C3")
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F, variant=variant)
+    assert nm <= len(cfg_g) * 1e-3  # index disagreements are rare (and all were ties)
+    st, sid, cfg, ob = s.best_set()
+    best_o = obj_o.max()
+    assert st == 0 and obj_o[sid] >= best_o * (1 - TAU_OBJ)
+
+
+def test_c3_greedy_allocation(cs):
+    pb, F = bench_config("C3")
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    st, ids, cfgs, tot = s.best_allocation(500)
+    assert st == 0 and len(ids) == 500
+    _, obj_o = Oracle(pb).score_range(F)
+    ok, why = replay_greedy(1000, 2, obj_o, ids)
+    assert ok, why
+    assert cfgs == [int(cfg_g[i]) for i in ids]
+    gk = [obj_g[i] for i in ids]
+    assert all(a >= b for a, b in zip(gk, gk[1:]))
+
+
+# ---- edge cases ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [2, 3, 31, 33, 65, 127, 130])
+def test_ragged_queue_sizes(cs, n):
+    pb = make_problem("b200", "c21", coef_seed=50 + n, alpha=0.62)
+    F, _ = make_features(n, seed=50 + n)
+    for variant in (0, 1):
+        _full_parity(cs, pb, F, variant=variant)
+
+
+def test_empty_and_single_job_queue(cs):
+    pb = make_problem("b200", "c10", coef_seed=3)
+    F, _ = make_features(1, seed=3)
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    assert len(cfg_g) == 0
+    st, sid, cfg, ob = s.best_set()
+    assert st == 2 and sid == -1
+
+
+def test_all_infeasible(cs):
+    pb = make_problem("b200", "c10", coef_seed=4, alpha=10.0)
+    F, _ = make_features(40, seed=4)
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    assert (cfg_g == -1).all() and np.all(obj_g == -np.inf)
+    assert s.best_set()[0] == 2
+    assert s.best_allocation(20)[0] == 2
+
+
+def test_jobs_indirection_with_repeats(cs):
+    pb = make_problem("b200", "c21", coef_seed=7, alpha=0.6)
+    F, _ = make_features(50, seed=7)
+    jobs = np.array([(i * 7) % 50 for i in range(70)], dtype=np.int32)  # repeats rows
+    _full_parity(cs, pb, F, jobs)
+
+
+def test_tie_stress_duplicates(cs):
+    """Duplicated jobs create exact ties between mirrored states: the lowest config must win."""
+    pb = make_problem("b200", "c21", coef_seed=8, alpha=0.2, mirror_ties=True)
+    F = tie_stress_features(120, seed=8, frac=0.25)
+    for variant in (0, 1):
+        s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F, variant=variant)
+
+
+def test_problem1_one_cap(cs):
+    pb = make_problem("b200", "c1_900", coef_seed=9, objective=1, alpha=0.3)
+    F, _ = make_features(90, seed=9)
+    _full_parity(cs, pb, F)
+
+
+def test_alpha_zero_and_high(cs):
+    for alpha in (0.0, 0.7):
+        pb = make_problem("b200", "c10", coef_seed=10, alpha=alpha)
+        F, _ = make_features(80, seed=10)
+        _full_parity(cs, pb, F)
+
+
+def test_triples_small(cs):
+    pb = make_problem("b200_3way", "c21", coef_seed=11, alpha=0.2)
+    F, _ = make_features(24, seed=11)
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F)
+    st, ids, cfgs, tot = s.best_allocation(8)  # greedy (24 > 15)
+    ok, why = replay_greedy(24, 3, obj_o, ids)
+    assert ok, why
+
+
+def test_triples_exact_allocation(cs):
+    pb = make_problem("b200_3way", "c10", coef_seed=12, alpha=0.2)
+    F, _ = make_features(9, seed=12)
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F)
+    st, ids, cfgs, tot = s.best_allocation(3)
+    ost, rank, oids, otot, nmatch = oracle.exact_allocation(9, 3, obj_o)
+    assert nmatch == 280 and st == ost == 0
+    assert ids == oids or sum(obj_o[i] for i in ids) >= otot * (1 - TAU_OBJ)
+
+
+def test_solo_normalisation(cs):
+    """A solo job on the full chip at P_max has RPerf exactly 1 (C = e6, D = 0)."""
+    pb = make_problem("solo", "c10", coef_seed=13, objective=1, alpha=0.0)
+    F, _ = make_features(64, seed=13)
+    s, obj_g, cfg_g, cfg_o, obj_o, nm = _full_parity(cs, pb, F)
+    for sid in (0, 17, 63):
+        d = s.best_config(sid)
+        if d["cap"] == pb.n_caps - 1:
+            assert d["rperf"][0] == 1.0
+
+
+def test_validation_errors(cs):
+    pb = make_problem("b200", "c10", coef_seed=14)
+    F, _ = make_features(20, seed=14)
+    for row, col, val, code in [(5, 0, 0.001, 13), (7, 3, 150.0, 14), (9, 2, float("nan"), 14)]:
+        G = F.copy()
+        G[row, col] = val
+        G[row + 3, 0] = 0.0  # a later bad job must not win
+        s = cs.Scheduler(pb)
+        s.score_all(torch.from_numpy(G).cuda())
+        with pytest.raises(cs.CoschedError) as e:
+            s.best_set()
+        assert e.value.status == code and f"job {row}" in str(e.value)
+        assert Oracle.validate_features(G)[0] == code
+
+
+def test_create_validation(cs):
+    bad = make_problem("b200", "c10", coef_seed=1)
+    bad.state_gpcs = bad.state_gpcs.copy()
+    bad.state_gpcs[0, 0] = 6
+    with pytest.raises(cs.CoschedError) as e:
+        cs.Scheduler(bad)
+    assert e.value.status == 11 and Oracle(bad).validate()[0] == 11
+    bad = make_problem("b200", "c10", coef_seed=1)
+    bad.state_slice = bad.state_slice.copy()
+    bad.state_slice[2, 1] = 40
+    with pytest.raises(cs.CoschedError) as e:
+        cs.Scheduler(bad)
+    assert e.value.status == 12
+
+
+# ---- multi-GPU sharding on one GPU (fake ranks) ---------------------------------------
+
+@pytest.mark.parametrize("W", [2, 3, 4, 8])
+def test_fake_ranks_equal_single_rank(cs, W):
+    pb = make_problem("b200", "c21", coef_seed=15, alpha=0.3)
+    F, _ = make_features(301, seed=15)
+    s1, obj1, cfg1 = _run(cs, pb, F)
+    key1 = s1.local_best_key()
+    Fd = torch.from_numpy(F).cuda()
+    keys, objs, cfgs = [], [], []
+    for r in range(W):
+        s = cs.Scheduler(pb)
+        s.set_shard_view(r, W)
+        o, c = s.score_all(Fd)
+        keys.append(s.local_best_key())
+        objs.append(o.cpu().numpy())
+        cfgs.append(c.cpu().numpy())
+    assert max(keys) == key1
+    assert np.array_equal(np.concatenate(cfgs), cfg1)
+    assert np.array_equal(np.concatenate(objs), obj1)
+
+
+# ---- full-size configs: sampled parity --------------------------------------------------
+
+def test_c4_full_size_sampled(cs):
+    pb, F = bench_config("C4")
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    n = 10000
+    rng = np.random.default_rng(2024)
+    sample = np.unique(np.concatenate([rng.integers(0, len(cfg_g), 3000), [0, len(cfg_g) - 1]]))
+    o = Oracle(pb)
+    exact, fails = check_sets(o, F, None, sample, cfg_g[sample], obj_g[sample], n, 2)
+    assert not fails, fails[:5]
+    assert exact >= 0.99 * len(sample)
+    st, sid, cfg, ob = s.best_set()
+    assert st == 0 and ob == obj_g.max() and sid == int(np.argmax(obj_g))
+    exact, fails = check_sets(o, F, None, [sid], [cfg], [ob], n, 2)
+    assert not fails, fails
+
+
+def test_c5_triples_sampled(cs):
+    pb, F = bench_config("C5")
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    rng = np.random.default_rng(2025)
+    sample = np.unique(rng.integers(0, len(cfg_g), 400))
+    exact, fails = check_sets(Oracle(pb), F, None, sample, cfg_g[sample], obj_g[sample], 2000, 3)
+    assert not fails, fails[:5]
+    st, sid, cfg, ob = s.best_set()
+    assert st == 0 and ob == obj_g.max()
