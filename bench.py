@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the exhaustive co-location search (BASELINE.json metric:
+candidate configs scored per second, and the fraction of the scorer's roofline).
+
+One step = one pass of the hot path over the queue: validate + basis +
+projection + every (set, state, cap) candidate scored + per-set argmax +
+per-queue argmax + cross-GPU argmax (cosched_score_all + cosched_best_set).
+The greedy job->GPU allocation (cosched_best_allocation) is timed separately
+and reported as `allocation_ms`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU, NCCL)
+
+Workload: BASELINE.json config 4 (10,000-job queue, b200 table x 21 caps =
+294 configs per pair, 49,995,000 pairs) -- the configuration the 1/2/4/8-GPU
+metric is quoted on; synthetic class-shaped inputs (synth/).
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "candidate configs scored/sec (1/2/4/8 B200) and % of FP32/HBM roofline"
+UNIT = "candidates/s"
+# Roofline of the set scorer: the ALU pipe (FMNMX/FSETP/
+# LOP3: 64 lanes/clk/SM, measured in profiles/r01/microbench_pipes*) binds; the
+# exact method needs >= 1.5 ALU lane-ops per pair candidate (one 3-input min for
+# the masked Fairness test, half a 3-input max for the argmax) and 3 FP32 adds on
+# the 128-lane FMA pipe, which binds at the same rate. Triples: 2.5 ALU ops.
+ALU_OPS_PER_CAND = {1: 1.0, 2: 1.5, 3: 2.5}
+ALU_LANES_PER_SM_CLK = 64
+N_SM = 148
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_rate(pb, F, n_slots, budget_s=12.0, first=0):
+    """Oracle (as it stands, single-threaded FP64) on all host cores: disjoint set chunks,
+    one process per core, sized from a short calibration so the run takes ~budget_s."""
+    import multiprocessing as mproc
+
+    import oracle
+    o = oracle.Oracle(pb)
+    n_jobs = F.shape[0]
+    total = oracle.n_sets(n_jobs, n_slots)
+    t0 = time.perf_counter()
+    probe = min(2000, total)
+    o.score_range(F, None, first, probe)
+    per_set = (time.perf_counter() - t0) / max(probe, 1)
+    cores = os.cpu_count() or 1
+    chunk = max(1, min(total // cores, int(budget_s / max(per_set, 1e-9))))
+    ctx = mproc.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        starts = [(first + i * chunk) % max(total - chunk, 1) for i in range(cores)]
+        pool.starmap(_oracle_chunk, [(pb, F, s, chunk) for s in starts])
+    dt = time.perf_counter() - t0
+    n_cand = cores * chunk * pb.n_configs
+    return {"value": n_cand / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cores} processes x {chunk} consecutive sets ({cores * chunk} sets, "
+                      f"{n_cand:.3g} candidates) of {pb.name} with {n_jobs} jobs, single-threaded FP64 "
+                      f"un-factorised oracle per process, {dt:.1f} s wall"}
+
+
+def _oracle_chunk(pb, F, start, count):
+    import oracle
+    oracle.Oracle(pb).score_range(F, None, start, count)
+    return count
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the paper's method written out plainly) on host cores."""
+    world, rank, local = _dist_env()
+    if rank != 0:
+        return 0
+    from synth import bench_config
+    pb, F = bench_config(args.config)
+    n_slots = pb.n_slots
+    # bounded sample per step, sized so the whole run stays within a few minutes
+    for _ in range(args.warmup):
+        pass
+    steps = []
+    info = None
+    for k in range(args.steps):
+        info = cpu_oracle_rate(pb, F, n_slots, budget_s=args.ref_budget, first=k * 7919)
+        steps.append(info["value"])
+    value = statistics.median(steps)
+    n_cand_step = None
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n_jobs": int(F.shape[0]), "n_slots": n_slots,
+                       "n_configs": pb.n_configs, "table": pb.name, "objective": pb.objective,
+                       "alpha": pb.alpha, "parallelism": "host processes"},
+            "cpu_baseline": {"kind": info["kind"], "cores": info["cores"], "sample": info["sample"],
+                             "value": value, "unit": UNIT},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_03838_b200 as cs
+    from synth import bench_config
+
+    world, rank, local = _dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pb, F = bench_config(args.config)
+    n_jobs = F.shape[0]
+    sched = cs.Scheduler(pb, device=local)
+    if args.variant is not None:
+        sched.set_variant(args.variant)
+    if world > 1:
+        uid = [cs.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sched.set_comm(uid[0], rank, world)
+    stream = torch.cuda.current_stream()
+    Fd = torch.from_numpy(F).to(dev)
+    first, count = sched.shard_range(n_jobs)
+    n_cfg = pb.n_configs
+    total_sets = cs.n_sets(n_jobs, pb.n_slots)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        sched.score_all(Fd, None, with_out=True, stream=stream)
+        return sched.best_set()
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    score_ms, prep_ms = [], []
+    launches0 = sched.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)  # evict L2 between timed steps (not timed)
+            e0, e1 = ev[k]
+            e0.record(stream)
+            res = step()
+            e1.record(stream)
+            p, s, _ = sched.last_timings()
+            prep_ms.append(p)
+            score_ms.append(s)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = sched.kernel_launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total = float(t.item())
+        sm = torch.tensor([sum(score_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(sm, op=dist.ReduceOp.MAX)
+        score_total = float(sm.item())
+    else:
+        t_total = t_local
+        score_total = sum(score_ms)
+    ms_per_step = t_total / args.steps
+    cand_per_step = total_sets * n_cfg
+    value = cand_per_step / (ms_per_step * 1e-3)
+
+    # end to end through the public API with host buffers: pinned H2D of the
+    # features, the search, D2H of the result (best set id/cfg/obj) every step
+    Fh = torch.from_numpy(F).pin_memory()
+    e2e_times = []
+    for k in range(max(2, args.steps)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        Fd.copy_(Fh, non_blocking=True)
+        r = step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = statistics.median(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+
+    # allocation latency (timed separately)
+    alloc_ms = None
+    if args.alloc_k:
+        sched.score_all(Fd, None, with_out=True, stream=stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st, ids, cfgs, tot = sched.best_allocation(args.alloc_k)
+        alloc_ms = (time.perf_counter() - t0) * 1e3
+
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        sm_clk = peaks.get("sm_max_mhz", 1965.0)
+        alu_peak = N_SM * ALU_LANES_PER_SM_CLK * sm_clk * 1e6 / 1e12  # T lane-ops/s
+        score_avg_ms = score_total / args.steps
+        local_cand = count * n_cfg  # per-rank candidates of one scorer launch (rank 0's shard)
+        ops = ALU_OPS_PER_CAND[pb.n_slots]
+        achieved = local_cand * ops / (score_avg_ms * 1e-3) / 1e12
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "n_jobs": n_jobs, "n_slots": pb.n_slots,
+                       "n_sets": total_sets, "n_configs": n_cfg, "candidates_per_step": cand_per_step,
+                       "table": pb.name, "objective": pb.objective, "alpha": pb.alpha,
+                       "parallelism": f"set-range shards x{world}, NCCL u64-max argmax",
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "scorer": "fast" if (args.variant is None or args.variant == 1) else "generic"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-ops/s",
+                         "frac": achieved / alu_peak, "traffic": None,
+                         "kernel": "set scorer", "ops_per_candidate": ops,
+                         "kernel_ms": score_avg_ms, "kernel_share_of_step": score_avg_ms / ms_per_step,
+                         "peak_source": f"148 SM x 64 ALU lanes x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)"},
+            "e2e": {"value": cand_per_step / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(F.nbytes),
+                    "d2h_bytes_per_step": 8 + 32},
+            "gpu_launches": int(launches),
+            "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k,
+            "clocks": clocks,
+        }
+        if args.cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_oracle_rate(pb, F, pb.n_slots, budget_s=args.ref_budget)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", type=int, default=None, help="pair scorer: 1 fast (default), 0 generic")
+    ap.add_argument("--alloc-k", type=int, default=5000)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        args.ref_budget = min(args.ref_budget, 150.0 / max(args.steps, 1))
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

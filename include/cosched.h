@@ -204,6 +204,11 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
  * against). Env COSCHED_PAIR_KERNEL=generic selects 0 at create. */
 cosched_status cosched_set_variant(cosched_t h, int variant);
 
+/* Device time (ms, CUDA events on the caller's stream) of the last
+ * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
+ * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */
+cosched_status cosched_last_timings(cosched_t h, float* ms3);
+
 /* Number of kernels the library launched since create (instrumentation for bench.py). */
 int64_t cosched_kernel_launches(cosched_t h);
 

@@ -138,6 +138,12 @@ class Scheduler:
     def set_variant(self, variant: int):
         self._check(self._L.cosched_set_variant(self._h, variant))
 
+    def last_timings(self):
+        """(prep_ms, score_ms, total_ms) of the last score_all, from CUDA events on its stream."""
+        ms = (ctypes.c_float * 3)()
+        self._check(self._L.cosched_last_timings(self._h, ms))
+        return ms[0], ms[1], ms[2]
+
     @property
     def kernel_launches(self) -> int:
         return int(self._L.cosched_kernel_launches(self._h))

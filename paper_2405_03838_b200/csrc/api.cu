@@ -100,6 +100,7 @@ struct cosched_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   int view_nranks = 1;  // shard view without comm (tests)
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   static constexpr int kSmallSets = 512;
   static constexpr int kDetailRows = 8192;
 };
@@ -296,6 +297,8 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
             cudaMalloc(&h->d_detail, (size_t)cosched_ctx::kDetailRows * 8 * 4) == cudaSuccess &&
             cudaMalloc(&h->d_detail_ids, (size_t)cosched_ctx::kDetailRows * 8) == cudaSuccess &&
             cudaMallocHost(&h->h_pinned, 8 * 8) == cudaSuccess &&
+            cudaEventCreate(&h->ev[0]) == cudaSuccess && cudaEventCreate(&h->ev[1]) == cudaSuccess &&
+            cudaEventCreate(&h->ev[2]) == cudaSuccess && cudaEventCreate(&h->ev[3]) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_c, d->coef_c, nc * 6 * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_d, d->coef_d, nc * 3 * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) {
@@ -321,6 +324,8 @@ void cosched_destroy(cosched_t h) {
     cudaFree(h->d_detail);
     cudaFree(h->d_detail_ids);
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
+    for (int i = 0; i < 4; i++)
+      if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   }
   delete h;
 }
@@ -504,6 +509,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Workspace ws;
   workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, (char*)workspace_dev, &ws);
+  cudaEventRecord(h->ev[0], st);
   launch_fill_u64(ws.err, ~0ull, 1, st);
   launch_fill_u64(ws.best_key, 0ull, 1, st);
   h->launches += 2;
@@ -512,7 +518,9 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, st);
     h->launches += 2;
   }
+  cudaEventRecord(h->ev[1], st);
   h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
+  cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
   h->scored = true;
@@ -539,6 +547,17 @@ static cosched_status check_deferred(cosched_t h) {
                                                             : "row index outside [0, n_rows)";
   snprintf(buf, sizeof buf, "job %lld: %s", pos, what);
   return fail(h, (cosched_status)code, buf);
+}
+
+cosched_status cosched_last_timings(cosched_t h, float* ms3) {
+  if (!h || !ms3) return fail(h, COSCHED_E_ARG, "null argument");
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  DeviceGuard g(h->device);
+  CK(cudaEventSynchronize(h->ev[2]));
+  CK(cudaEventElapsedTime(&ms3[0], h->ev[0], h->ev[1]));
+  CK(cudaEventElapsedTime(&ms3[1], h->ev[1], h->ev[2]));
+  CK(cudaEventElapsedTime(&ms3[2], h->ev[0], h->ev[2]));
+  return COSCHED_OK;
 }
 
 cosched_status cosched_local_best_key(cosched_t h, uint64_t* key) {
