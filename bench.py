@@ -274,12 +274,14 @@ def run_ours(args):
 
     # allocation latency (timed separately)
     alloc_ms = None
+    alloc_rounds = None
     if args.alloc_k:
         sched.score_all(Fd, None, with_out=True, stream=stream)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st, ids, cfgs, tot = sched.best_allocation(args.alloc_k)
         alloc_ms = (time.perf_counter() - t0) * 1e3
+        alloc_rounds = sched.greedy_rounds
 
     if rank == 0:
         peaks, peak_src = _peaks()
@@ -308,7 +310,7 @@ def run_ours(args):
             "e2e": {"value": cand_per_step / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(F.nbytes),
                     "d2h_bytes_per_step": 8 + 32},
             "gpu_launches": int(launches),
-            "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k,
+            "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k, "allocation_rounds": alloc_rounds,
             "clocks": clocks,
         }
         if args.cpu_baseline and world == 1:

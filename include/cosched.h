@@ -209,6 +209,9 @@ cosched_status cosched_set_variant(cosched_t h, int variant);
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */
 cosched_status cosched_last_timings(cosched_t h, float* ms3);
 
+/* Rounds of the last greedy cosched_best_allocation (instrumentation). */
+int64_t cosched_last_greedy_rounds(cosched_t h);
+
 /* Number of kernels the library launched since create (instrumentation for bench.py). */
 int64_t cosched_kernel_launches(cosched_t h);
 

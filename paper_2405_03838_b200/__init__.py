@@ -145,6 +145,10 @@ class Scheduler:
         return ms[0], ms[1], ms[2]
 
     @property
+    def greedy_rounds(self) -> int:
+        return int(self._L.cosched_last_greedy_rounds(self._h))
+
+    @property
     def kernel_launches(self) -> int:
         return int(self._L.cosched_kernel_launches(self._h))
 

@@ -58,6 +58,7 @@ SIGNATURES = [
     ("cosched_set_shard_view", I32, [P, ctypes.c_int, ctypes.c_int]),
     ("cosched_last_timings", I32, [P, P]),
     ("cosched_kernel_launches", I64, [P]),
+    ("cosched_last_greedy_rounds", I64, [P]),
 ]
 
 _lib = None

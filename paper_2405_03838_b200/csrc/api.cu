@@ -100,6 +100,7 @@ struct cosched_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   int view_nranks = 1;  // shard view without comm (tests)
+  int64_t greedy_rounds = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   static constexpr int kSmallSets = 512;
   static constexpr int kDetailRows = 8192;
@@ -129,18 +130,22 @@ float unord_float(uint32_t o) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t np, int64_t n_sets_local, char* base,
-                        Workspace* ws) {
+int64_t pad_jobs(int64_t n_jobs) { return (n_jobs + 63) / 64 * 64; }
+
+size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
+                        int64_t n_sets_local, char* base, Workspace* ws) {
   size_t off = 0;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + off : nullptr;
     off += align256(bytes);
     return p;
   };
-  size_t proj = (size_t)n_jobs * n_slices * np * sizeof(float);
+  const size_t jp = (size_t)pad_jobs(n_jobs);
+  size_t proj = jp * n_slices * rs * sizeof(float);
   Workspace w;
   w.ka = (float*)take(proj);
   w.kb = (float*)take(proj);
+  w.w = (float*)take(jp * n_slots * n_states * rs * sizeof(float));
   w.best_key = (unsigned long long*)take(8);
   w.err = (unsigned long long*)take(8);
   w.counters = (int64_t*)take(8 * 8);
@@ -273,13 +278,13 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
   sp.n_slices = d->n_slices;
   sp.n_caps = d->n_caps;
   sp.np = (d->n_caps + 3) & ~3;
+  sp.rs = ((sp.np >> 2) & 1) ? sp.np : sp.np + 4;
+  sp.n_jobs_pad = 0;
   sp.n_cfg = d->n_states * d->n_caps;
   sp.alpha = d->alpha;
-  const float nalpha = (float)d->n_slots * d->alpha;
   for (int p = 0; p < d->n_caps; p++) {
     float inv = d->objective == 2 ? 1.0f / d->caps_w[p] : 1.0f;
-    sp.obj_scale[p] = inv * kInvScale;  // exact power-of-two rescale of fl(1/P)
-    sp.obj_bias[p] = nalpha * inv;
+    sp.inv_p[p] = inv;
   }
   for (int s = 0; s < d->n_states; s++)
     for (int i = 0; i < d->n_slots; i++) sp.slice[s][i] = (int16_t)d->state_slice[s * d->n_slots + i];
@@ -333,6 +338,8 @@ void cosched_destroy(cosched_t h) {
 const char* cosched_last_error(cosched_t h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
 int64_t cosched_kernel_launches(cosched_t h) { return h ? h->launches : 0; }
+
+int64_t cosched_last_greedy_rounds(cosched_t h) { return h ? h->greedy_rounds : 0; }
 
 cosched_status cosched_set_variant(cosched_t h, int variant) {
   if (!h || variant < 0 || variant > 1) return COSCHED_E_ARG;
@@ -414,7 +421,7 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
   if (!h || !bytes || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad workspace_size arguments");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, nullptr, nullptr);
+  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, nullptr, nullptr);
   return COSCHED_OK;
 }
 
@@ -494,7 +501,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     return fail(h, COSCHED_E_ARG, "queue too large: more than 2^32-2 sets");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, nullptr, nullptr);
+  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, nullptr, nullptr);
   if (!workspace_dev || workspace_bytes < need || ((uintptr_t)workspace_dev & 255))
     return fail(h, COSCHED_E_OOM, "workspace missing, misaligned or smaller than cosched_workspace_size");
   float* obj = nullptr;
@@ -508,18 +515,19 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   DeviceGuard g(h->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Workspace ws;
-  workspace_layout(n_jobs, h->sp.n_slices, h->sp.np, count, (char*)workspace_dev, &ws);
+  workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, (char*)workspace_dev, &ws);
+  h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
   launch_fill_u64(ws.err, ~0ull, 1, st);
   launch_fill_u64(ws.best_key, 0ull, 1, st);
   h->launches += 2;
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, st);
-    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, st);
+    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, st);
     h->launches += 2;
   }
   cudaEventRecord(h->ev[1], st);
-  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
+  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
   cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
@@ -577,7 +585,7 @@ static cosched_status detail_rows(cosched_t h, const int64_t* ids, int64_t n, st
   for (int64_t off = 0; off < n; off += cosched_ctx::kDetailRows) {
     int64_t m = std::min<int64_t>(cosched_ctx::kDetailRows, n - off);
     CK(cudaMemcpyAsync(h->d_detail_ids, ids + off, m * 8, cudaMemcpyHostToDevice, h->stream));
-    launch_sets_detail(h->sp, h->ws.ka, h->ws.kb, h->d_detail_ids, m, h->d_detail, h->stream);
+    launch_sets_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->d_detail_ids, m, h->d_detail, h->stream);
     h->launches++;
     CK(cudaMemcpyAsync(rows->data() + off * 8, h->d_detail, m * 8 * 4, cudaMemcpyDeviceToHost, h->stream));
   }
@@ -661,7 +669,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     // score every set of the (tiny) queue locally: no collective needed
     int64_t all = cosched::n_sets(N, ns);
     launch_fill_u64(h->d_small_key, 0ull, 2, h->stream);
-    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, 0, all, h->d_small_obj, h->d_small_cfg,
+    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, 0, all, h->d_small_obj, h->d_small_cfg,
                                     h->d_small_key, h->ws.err, h->variant, h->stream);
     int64_t nm = n_partitions(ns, N);
     launch_exact_alloc(ns, N, h->d_small_obj, nm, h->d_small_key + 1, h->stream);
@@ -691,14 +699,44 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
   int64_t* cnt = ws.counters;  // [0] n_alive, [1] n_picked, [2] n_alive2
   launch_fill_u64((unsigned long long*)cnt, 0ull, 8, h->stream);
   launch_fill_u32(ws.taken, 0u, N, h->stream);
+  h->launches += 2;
+  int64_t host_cnt[8];
+  int64_t n_picked = 0;
+  h->greedy_rounds = 0;
+  if (ns == 2) {
+    // pairs: tile-scan propose + per-job select; picks are identical on every rank
+    auto c2 = [](int64_t n) { return n * (n - 1) / 2; };
+    int64_t c0 = 0, c1 = 0;
+    while (c2(c0 + 1) <= h->first && c0 < N) c0++;
+    if (c2(c0) != h->first) c0 = 0;
+    c1 = c0;
+    while (c1 < N && c2(c1 + 1) <= h->first + h->n_sets) c1++;
+    if (h->n_sets > 0) c1 = std::max(c1, c0 + 1);
+    for (int round = 0; round < 1000000; round++) {
+      launch_fill_u64(ws.job_key, 0ull, N, h->stream);
+      launch_greedy_pairs_propose(h->out_obj, h->first, c0, c1, ws.taken, ws.job_key, h->stream);
+      h->launches += 2;
+      st = allreduce_max(h, ws.job_key, N, kNcclUint64);
+      if (st != COSCHED_OK) return st;
+      launch_greedy_pairs_select(ws.job_key, N, ws.picked, cnt + 1, h->stream);
+      h->launches++;
+      CK(cudaMemcpyAsync(host_cnt, cnt, 64, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      int64_t now = host_cnt[1];
+      h->greedy_rounds++;
+      if (now == n_picked) break;
+      launch_greedy_mark(2, ws.picked, n_picked, now, ws.taken, h->stream);
+      h->launches++;
+      n_picked = now;
+    }
+  } else {
   launch_greedy_init(ns, N, h->out_obj, h->first, h->n_sets, ws.alive, cnt + 0, h->stream);
-  h->launches += 3;
+  h->launches += 1;
   int64_t* alive = ws.alive;
   int64_t* alive2 = ws.alive2;
-  int64_t host_cnt[8];
   CK(cudaMemcpyAsync(host_cnt, cnt, 64, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  int64_t n_alive = host_cnt[0], n_picked = 0;
+  int64_t n_alive = host_cnt[0];
   for (int round = 0; round < 1000000; round++) {
     int64_t any_alive = n_alive;
     if (h->nranks > 1) {
@@ -710,6 +748,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
       CK(cudaStreamSynchronize(h->stream));
     }
     if (any_alive == 0) break;
+    h->greedy_rounds++;
     launch_fill_u64(ws.job_key, 0ull, N, h->stream);
     launch_greedy_propose(ns, N, h->out_obj, h->first, alive, n_alive, ws.taken, ws.job_key, h->stream);
     h->launches += 2;
@@ -733,6 +772,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     n_alive = host_cnt[2];
     std::swap(alive, alive2);
   }
+  }
   // gather picks: per-job key of the set that took it, max over ranks
   launch_fill_u64(ws.job_key, 0ull, N, h->stream);
   h->launches++;
@@ -742,7 +782,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     CK(cudaStreamSynchronize(h->stream));
   }
   std::vector<unsigned long long> all_keys;
-  if (h->nranks > 1) {
+  if (h->nranks > 1 && ns != 2) {
     // job_key[j] = key of the set containing j (a set's key lands on each of its jobs)
     std::vector<unsigned long long> jk(N, 0ull);
     for (unsigned long long key : mine) {

@@ -30,11 +30,13 @@ struct SpaceParams {
   int32_t n_states;
   int32_t n_slices;
   int32_t n_caps;
-  int32_t np;                 // caps padded to a multiple of 4 (row length of the projection)
+  int32_t np;                 // caps padded to a multiple of 4
+  int32_t rs;                 // row stride of the projection rows (floats): np, or np+4 when np/4 is even,
+                              // so 8 consecutive rows fall in distinct 16-byte shared-memory bank groups
+  int64_t n_jobs_pad;         // jobs rounded up to a multiple of 64 (rows of every projection block)
   int32_t n_cfg;              // n_states * n_caps
   float alpha;
-  float obj_scale[kMaxCaps];  // per cap: invP/K (Problem 2) or 1/K (Problem 1)
-  float obj_bias[kMaxCaps];   // per cap: n_slots*alpha*invP (Problem 2) or n_slots*alpha (Problem 1)
+  float inv_p[kMaxCaps];      // per cap: fl(1/P) (Problem 2) or 1 (Problem 1)
   int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
 };
 
@@ -46,8 +48,11 @@ struct DeviceTables {
 
 // Workspace layout (carved from the caller's buffer, all 256-byte aligned).
 struct Workspace {
-  float* ka = nullptr;              // [n_jobs][n_slices][np] = K*(U - alpha); padding = -1e30
-  float* kb = nullptr;              // [n_jobs][n_slices][np] = K*V;           padding = -1e30
+  float* ka = nullptr;              // [n_slices][n_jobs_pad][rs] = K*(U - alpha); padding = -1e30
+  float* kb = nullptr;              // [n_slices][n_jobs_pad][rs] = K*V;           padding = -1e30
+  float* w = nullptr;               // [n_slots][n_states][n_jobs_pad][rs] throughput share of the job in
+                                    //   slot i of state s at cap p, already divided by P (Problem 2):
+                                    //   (U[s_i] + sum_{l != i} V[s_l]) * invP; padding = -1e30
   unsigned long long* best_key = nullptr;  // [1] shard argmax key
   unsigned long long* err = nullptr;       // [1] first bad job: (pos << 8) | status, ~0 = none
   unsigned long long* job_key = nullptr;   // [n_jobs] greedy per-job best keys
@@ -59,17 +64,19 @@ struct Workspace {
   size_t bytes = 0;
 };
 
-size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t np, int64_t n_sets_local, char* base,
-                        Workspace* ws);
+size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
+                        int64_t n_sets_local, char* base, Workspace* ws);
+int64_t pad_jobs(int64_t n_jobs);
 
 // ---- kernel launchers (defined in kernels.cu) ------------------------------------
 void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
                      unsigned long long* err, cudaStream_t st);
 void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
-                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, cudaStream_t st);
+                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
+                    cudaStream_t st);
 // Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
 // maxes the packed key into *best_key. Returns the number of kernels launched.
-int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb,
+int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                  const unsigned long long* err, int variant, cudaStream_t st);
 void launch_exact_alloc(int n_slots, int64_t n_jobs, const float* set_obj, int64_t n_match,
@@ -87,10 +94,15 @@ void launch_greedy_select(int n_slots, int64_t n_jobs, const float* obj, int64_t
 void launch_greedy_mark(int n_slots, const unsigned long long* picked, int64_t from, int64_t to, uint32_t* taken,
                         cudaStream_t st);
 void launch_sort_keys_desc(const unsigned long long* keys, int64_t n, unsigned long long* sorted, cudaStream_t st);
-void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const int64_t* set_ids, int64_t n,
+void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
+                        int64_t n,
                         float* out /* [n][4 + kMaxSlots] */, cudaStream_t st);
 void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive,
                            const uint32_t* taken, int64_t* alive_out, int64_t* n_out, cudaStream_t st);
+void launch_greedy_pairs_propose(const float* obj, int64_t first, int64_t c0, int64_t c1, const uint32_t* taken,
+                                 unsigned long long* job_key, cudaStream_t st);
+void launch_greedy_pairs_select(const unsigned long long* job_key, int64_t n_jobs, unsigned long long* picked,
+                                int64_t* n_picked, cudaStream_t st);
 void launch_fill_u64(unsigned long long* p, unsigned long long v, int64_t n, cudaStream_t st);
 void launch_fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t st);
 

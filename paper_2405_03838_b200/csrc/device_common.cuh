@@ -22,6 +22,17 @@ __device__ __forceinline__ void basis_hj(const float* __restrict__ f, float h[6]
   j[2] = 1.0f;
 }
 
+// Projection rows (slice-major, padded; see Workspace in cosched_internal.h)
+template <typename SP>
+__device__ __forceinline__ const float* ka_row(const float* __restrict__ base, const SP& sp, int slice, int64_t job) {
+  return base + ((int64_t)slice * sp.n_jobs_pad + job) * sp.rs;
+}
+template <typename SP>
+__device__ __forceinline__ const float* w_row(const float* __restrict__ base, const SP& sp, int slot, int state,
+                                              int64_t job) {
+  return base + (((int64_t)slot * sp.n_states + state) * sp.n_jobs_pad + job) * sp.rs;
+}
+
 // order-preserving float -> u32 (larger float <=> larger u32; -0 < +0)
 __device__ __forceinline__ uint32_t ord_float_d(float f) {
   uint32_t b = __float_as_uint(f);

@@ -58,19 +58,32 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
 //   U = C[p][s] . H(F_n),  V = D[p][s] . J(F_n)   (the two dot products of P:L458)
 //   ka = K*(U - alpha),   kb = K*V               (exact power-of-two scaling)
 // Padding caps (p >= n_caps) get -1e30 so every candidate using them is infeasible.
+__device__ __forceinline__ float dot_u(const float* __restrict__ C, const float h[6]) {
+  float u = __fmul_rn(C[0], h[0]);
+#pragma unroll
+  for (int t = 1; t < 6; t++) u = __fmaf_rn(C[t], h[t], u);
+  return u;
+}
+__device__ __forceinline__ float dot_v(const float* __restrict__ D, const float j[3]) {
+  float v = __fmul_rn(D[0], j[0]);
+#pragma unroll
+  for (int t = 1; t < 3; t++) v = __fmaf_rn(D[t], j[t], v);
+  return v;
+}
+
 __global__ void k_project(const float* __restrict__ F, const int32_t* __restrict__ jobs, int64_t n_jobs,
                           const SpaceParams sp, const float* __restrict__ coef_c,
                           const float* __restrict__ coef_d, const unsigned long long* __restrict__ err,
                           float* __restrict__ ka, float* __restrict__ kb) {
   if (*err != ~0ull) return;  // invalid input: leave the workspace untouched
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t total = n_jobs * sp.n_slices * sp.np;
+  int64_t total = (int64_t)sp.n_slices * sp.n_jobs_pad * sp.rs;
   if (idx >= total) return;
-  int p = (int)(idx % sp.np);
-  int64_t ns = idx / sp.np;
-  int s = (int)(ns % sp.n_slices);
-  int64_t n = ns / sp.n_slices;
-  if (p >= sp.n_caps) {
+  int p = (int)(idx % sp.rs);
+  int64_t r = idx / sp.rs;
+  int64_t n = r % sp.n_jobs_pad;
+  int s = (int)(r / sp.n_jobs_pad);
+  if (p >= sp.n_caps || n >= n_jobs) {
     ka[idx] = -1e30f;
     kb[idx] = -1e30f;
     return;
@@ -78,39 +91,68 @@ __global__ void k_project(const float* __restrict__ F, const int32_t* __restrict
   int64_t row = jobs ? (int64_t)jobs[n] : n;
   float h[6], j[3];
   basis_hj(F + row * 8, h, j);
-  const float* C = coef_c + ((int64_t)p * sp.n_slices + s) * 6;
-  const float* D = coef_d + ((int64_t)p * sp.n_slices + s) * 3;
-  float u = __fmul_rn(C[0], h[0]);
-#pragma unroll
-  for (int t = 1; t < 6; t++) u = __fmaf_rn(C[t], h[t], u);
-  float v = __fmul_rn(D[0], j[0]);
-#pragma unroll
-  for (int t = 1; t < 3; t++) v = __fmaf_rn(D[t], j[t], v);
+  float u = dot_u(coef_c + ((int64_t)p * sp.n_slices + s) * 6, h);
+  float v = dot_v(coef_d + ((int64_t)p * sp.n_slices + s) * 3, j);
   ka[idx] = __fmul_rn(__fsub_rn(u, sp.alpha), kScale);
   kb[idx] = __fmul_rn(v, kScale);
 }
 
+// Throughput share of job n when it sits in slot i of state s at cap p. The
+// model's Throughput = sum_i RPerf_i = sum_i (U[j_i][s_i] + sum_{l!=i} V[j_l][s_i])
+// regroups exactly per job as sum_i (U[j_i][s_i] + sum_{l!=i} V[j_i][s_l]), so
+//   w[n][i][s][p] = (U_n[s_i] + sum_{l != i} V_n[s_l]) * invP   (left-to-right sums)
+// and a candidate's objective is the FP32 sum of its jobs' shares in slot order.
+__global__ void k_project_w(const float* __restrict__ F, const int32_t* __restrict__ jobs, int64_t n_jobs,
+                            const SpaceParams sp, const float* __restrict__ coef_c,
+                            const float* __restrict__ coef_d, const unsigned long long* __restrict__ err,
+                            float* __restrict__ w) {
+  if (*err != ~0ull) return;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)sp.n_slots * sp.n_states * sp.n_jobs_pad * sp.rs;
+  if (idx >= total) return;
+  int p = (int)(idx % sp.rs);
+  int64_t r = idx / sp.rs;
+  int64_t n = r % sp.n_jobs_pad;
+  r /= sp.n_jobs_pad;
+  int s = (int)(r % sp.n_states);
+  int i = (int)(r / sp.n_states);
+  if (p >= sp.n_caps || n >= n_jobs) {
+    w[idx] = -1e30f;
+    return;
+  }
+  int64_t row = jobs ? (int64_t)jobs[n] : n;
+  float h[6], j[3];
+  basis_hj(F + row * 8, h, j);
+  float acc = dot_u(coef_c + ((int64_t)p * sp.n_slices + sp.slice[s][i]) * 6, h);
+  for (int l = 0; l < sp.n_slots; l++)
+    if (l != i) acc = __fadd_rn(acc, dot_v(coef_d + ((int64_t)p * sp.n_slices + sp.slice[s][l]) * 3, j));
+  w[idx] = __fmul_rn(acc, sp.inv_p[p]);
+}
+
 void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
-                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb,
+                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
                     cudaStream_t st) {
-  int64_t total = n_jobs * sp.n_slices * sp.np;
-  if (total <= 0) return;
+  int64_t total = (int64_t)sp.n_slices * sp.n_jobs_pad * sp.rs;
+  if (n_jobs <= 0 || total <= 0) return;
   int bs = 256;
   k_project<<<(unsigned)((total + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
                                                                err, ka, kb);
+  int64_t tw = (int64_t)sp.n_slots * sp.n_states * sp.n_jobs_pad * sp.rs;
+  k_project_w<<<(unsigned)((tw + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
+                                                              err, w);
 }
 
 // ---------------------------------------------------------------------------
 // a4-a8, generic reference scorer: one thread per set. For each config in
 // canonical order (state in table order, caps ascending):
 //   r_i'' = ka[j_i][s_i][p] + sum_{l != i} kb[j_l][s_i][p]   (= K*(RPerf_i - alpha))
-//   t     = sum_i r_i''
-//   obj   = fma(t, obj_scale[p], obj_bias[p])                (= Throughput [/ P])
+//   obj   = sum_i w[j_i][i][s][p]                          (= Throughput [/ P])
 //   feasible iff every r_i'' > 0  (Fairness > alpha)
 // keep the first strictly greater feasible obj.
 template <int NS>
 __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int64_t n_jobs,
                                                        const float* __restrict__ ka, const float* __restrict__ kb,
+                                                       const float* __restrict__ w,
                                                        int64_t first, int64_t count, float* __restrict__ out_obj,
                                                        int32_t* __restrict__ out_cfg,
                                                        unsigned long long* __restrict__ best_key,
@@ -122,21 +164,22 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
     int64_t sid = first + k;
     int64_t j[3];
     unrank_set<NS>(sid, j);
-    const int64_t row = (int64_t)sp.n_slices * sp.np;
     float best = -INFINITY;
     int32_t bc = -1;
     for (int s = 0; s < sp.n_states; s++) {
       const float* a[NS];
       const float* b[NS][NS];
+      const float* ww[NS];
 #pragma unroll
       for (int i = 0; i < NS; i++) {
         int sl = sp.slice[s][i];
-        a[i] = ka + j[i] * row + (int64_t)sl * sp.np;
+        a[i] = ka_row(ka, sp, sl, j[i]);
+        ww[i] = w_row(w, sp, i, s, j[i]);
 #pragma unroll
-        for (int l = 0; l < NS; l++) b[i][l] = kb + j[l] * row + (int64_t)sl * sp.np;
+        for (int l = 0; l < NS; l++) b[i][l] = ka_row(kb, sp, sl, j[l]);
       }
       for (int p = 0; p < sp.n_caps; p++) {
-        float t = 0.0f;
+        float o = 0.0f;
         bool feas = true;
 #pragma unroll
         for (int i = 0; i < NS; i++) {
@@ -145,11 +188,10 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
           for (int l = 0; l < NS; l++)
             if (l != i) r = __fadd_rn(r, b[i][l][p]);
           feas = feas && (r > 0.0f);
-          t = (i == 0) ? r : __fadd_rn(t, r);
+          o = (i == 0) ? ww[i][p] : __fadd_rn(o, ww[i][p]);
         }
-        float u = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
-        if (feas && u > best) {
-          best = u;
+        if (feas && o > best) {
+          best = o;
           bc = s * sp.n_caps + p;
         }
       }
@@ -161,24 +203,24 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
   block_max_key(key, best_key);
 }
 
-int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, int64_t first,
-                            int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
+                            int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                             const unsigned long long* err, cudaStream_t st);
 
-int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, int64_t first,
-                 int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
+                 int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                  const unsigned long long* err, int variant, cudaStream_t st) {
   if (count <= 0) return 0;
   if (variant != 0 && sp.n_slots == 2)
-    return launch_score_pairs_fast(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err, st);
+    return launch_score_pairs_fast(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, st);
   int bs = 256;
   unsigned grid = (unsigned)((count + bs - 1) / bs);
   if (sp.n_slots == 1)
-    k_score_generic<1><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+    k_score_generic<1><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err);
   else if (sp.n_slots == 2)
-    k_score_generic<2><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+    k_score_generic<2><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err);
   else
-    k_score_generic<3><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, first, count, obj, cfg, best_key, err);
+    k_score_generic<3><<<grid, bs, 0, st>>>(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err);
   return 1;
 }
 
@@ -189,7 +231,7 @@ int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const f
 // (RPerf_i = r_i''/K + alpha).
 // out row (8 floats): [0] cfg (int bits, -1 none), [1] obj, [2] thr, [3] fair, [4..] rperf
 __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
-                              const int64_t* __restrict__ set_ids, float* out_all) {
+                              const float* __restrict__ w, const int64_t* __restrict__ set_ids, float* out_all) {
   __shared__ unsigned long long s_key[32];
   const int64_t set_id = set_ids[blockIdx.x];
   float* out = out_all + (int64_t)blockIdx.x * 8;
@@ -197,21 +239,20 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
   if (sp.n_slots == 1) unrank_set<1>(set_id, j);
   else if (sp.n_slots == 2) unrank_set<2>(set_id, j);
   else unrank_set<3>(set_id, j);
-  const int64_t row = (int64_t)sp.n_slices * sp.np;
   unsigned long long key = 0;
   for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
     int s = c / sp.n_caps, p = c % sp.n_caps;
-    float t = 0.0f;
+    float u = 0.0f;
     bool feas = true;
     for (int i = 0; i < sp.n_slots; i++) {
       int sl = sp.slice[s][i];
-      float r = ka[j[i] * row + (int64_t)sl * sp.np + p];
+      float r = ka_row(ka, sp, sl, j[i])[p];
       for (int l = 0; l < sp.n_slots; l++)
-        if (l != i) r = __fadd_rn(r, kb[j[l] * row + (int64_t)sl * sp.np + p]);
+        if (l != i) r = __fadd_rn(r, ka_row(kb, sp, sl, j[l])[p]);
       feas = feas && (r > 0.0f);
-      t = (i == 0) ? r : __fadd_rn(t, r);
+      float wi = w_row(w, sp, i, s, j[i])[p];
+      u = (i == 0) ? wi : __fadd_rn(u, wi);
     }
-    float u = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
     unsigned long long kk = feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
     key = kk > key ? kk : key;
   }
@@ -229,29 +270,30 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
     }
     int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
     int s = c / sp.n_caps, p = c % sp.n_caps;
-    float thr = 0.0f, fair = INFINITY, t = 0.0f;
+    float thr = 0.0f, fair = INFINITY, u = 0.0f;
     for (int i = 0; i < sp.n_slots; i++) {
       int sl = sp.slice[s][i];
-      float r = ka[j[i] * row + (int64_t)sl * sp.np + p];
+      float r = ka_row(ka, sp, sl, j[i])[p];
       for (int l = 0; l < sp.n_slots; l++)
-        if (l != i) r = __fadd_rn(r, kb[j[l] * row + (int64_t)sl * sp.np + p]);
-      t = (i == 0) ? r : __fadd_rn(t, r);
+        if (l != i) r = __fadd_rn(r, ka_row(kb, sp, sl, j[l])[p]);
+      float wi = w_row(w, sp, i, s, j[i])[p];
+      u = (i == 0) ? wi : __fadd_rn(u, wi);
       float rp = __fmaf_rn(r, kInvScale, sp.alpha);
       out[4 + i] = rp;
       thr = (i == 0) ? rp : __fadd_rn(thr, rp);
       fair = fminf(fair, rp);
     }
     out[0] = __int_as_float(c);
-    out[1] = __fmaf_rn(t, sp.obj_scale[p], sp.obj_bias[p]);
+    out[1] = u;
     out[2] = thr;
     out[3] = fair;
   }
 }
 
-void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const int64_t* set_ids, int64_t n,
-                        float* out, cudaStream_t st) {
+void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
+                        int64_t n, float* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, set_ids, out);
+  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, out);
 }
 
 // Rank sort of a short list of unique keys, descending: position of key i =
@@ -501,6 +543,90 @@ void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, in
   if (n_slots == 1) k_greedy_compact<1><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
   else if (n_slots == 2) k_greedy_compact<2><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
   else k_greedy_compact<3><<<g, 256, 0, st>>>(alive, n_alive, taken, alive_out, n_out);
+}
+
+// ---------------------------------------------------------------------------
+// Greedy rounds for pairs without atomics per set: the shard's per-set
+// objectives form the upper triangle of an N x N matrix stored column by
+// column (colex: column j1 holds rows 0..j1-1 contiguously). A block scans a
+// 64 x 64 tile with coalesced column segments, reduces row and column maxima
+// of the free-pair keys in shared memory and issues one atomicMax per row and
+// column of the tile. Selection is then per job (O(N)): a pair is taken iff it
+// is the best free pair of both its jobs. Every rank derives the same picks
+// from the all-reduced job_key, so no taken[] exchange is needed.
+__global__ void __launch_bounds__(256) k_greedy_pairs_propose(const float* __restrict__ obj, int64_t first,
+                                                              int64_t c0, int64_t c1, int64_t jt0, int64_t base,
+                                                              int64_t n_tiles, const uint32_t* __restrict__ taken,
+                                                              unsigned long long* job_key) {
+  __shared__ unsigned long long s_row[4][64];
+  __shared__ unsigned long long s_col[64];
+  const int64_t t = blockIdx.x;
+  if (t >= n_tiles) return;
+  int64_t u = t + base;
+  int64_t J = (int64_t)((sqrt(8.0 * (double)u + 1.0) - 1.0) * 0.5);
+  while (J * (J + 1) / 2 > u) J--;
+  while ((J + 1) * (J + 2) / 2 <= u) J++;
+  const int64_t I = u - J * (J + 1) / 2;
+  const int lane_row = threadIdx.x & 63, cg = threadIdx.x >> 6;
+  const int64_t j0 = I * 64 + lane_row;
+  if (threadIdx.x < 64) s_col[threadIdx.x] = 0ull;
+  __syncthreads();
+  const bool row_free = j0 < c1 && taken[j0] == 0;
+  unsigned long long rbest = 0ull;
+  for (int k = 0; k < 16; k++) {
+    const int cl = cg + 4 * k;
+    const int64_t j1 = J * 64 + cl;
+    unsigned long long kk = 0ull;
+    if (row_free && j0 < j1 && j1 >= c0 && j1 < c1 && taken[j1] == 0) {
+      const int64_t sid = j1 * (j1 - 1) / 2 + j0;
+      const float o = obj[sid - first];
+      if (o > -INFINITY) kk = pack_key(o, sid);
+    }
+    rbest = kk > rbest ? kk : rbest;
+    unsigned long long cm = warp_max_u64(kk);  // a warp = 32 rows of one column
+    if ((threadIdx.x & 31) == 0 && cm) atomicMax(&s_col[cl], cm);
+  }
+  s_row[cg][lane_row] = rbest;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    unsigned long long r = s_row[0][threadIdx.x];
+    for (int q = 1; q < 4; q++) r = s_row[q][threadIdx.x] > r ? s_row[q][threadIdx.x] : r;
+    const int64_t jr = I * 64 + threadIdx.x;
+    if (r && job_key[jr] < r) atomicMax(&job_key[jr], r);
+    const unsigned long long c = s_col[threadIdx.x];
+    const int64_t jc = J * 64 + threadIdx.x;
+    if (c && job_key[jc] < c) atomicMax(&job_key[jc], c);
+  }
+}
+
+__global__ void k_greedy_pairs_select(const unsigned long long* __restrict__ job_key, int64_t n_jobs,
+                                      unsigned long long* picked, int64_t* n_picked) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n_jobs) return;
+  const unsigned long long key = job_key[j];
+  if (!key) return;
+  const int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+  int64_t jj[2];
+  unrank_set<2>(sid, jj);
+  if (jj[0] != j) return;  // the lower job of the pair decides
+  if (job_key[jj[1]] != key) return;
+  int64_t at = (int64_t)atomicAdd((unsigned long long*)n_picked, 1ull);
+  picked[at] = key;
+}
+
+void launch_greedy_pairs_propose(const float* obj, int64_t first, int64_t c0, int64_t c1, const uint32_t* taken,
+                                 unsigned long long* job_key, cudaStream_t st) {
+  if (c1 <= c0) return;
+  int64_t jt0 = c0 / 64, jt1 = (c1 - 1) / 64;
+  int64_t base = jt0 * (jt0 + 1) / 2;
+  int64_t n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - base;
+  k_greedy_pairs_propose<<<(unsigned)n_tiles, 256, 0, st>>>(obj, first, c0, c1, jt0, base, n_tiles, taken, job_key);
+}
+
+void launch_greedy_pairs_select(const unsigned long long* job_key, int64_t n_jobs, unsigned long long* picked,
+                                int64_t* n_picked, cudaStream_t st) {
+  if (n_jobs <= 0) return;
+  k_greedy_pairs_select<<<(unsigned)((n_jobs + 255) / 256), 256, 0, st>>>(job_key, n_jobs, picked, n_picked);
 }
 
 // ---------------------------------------------------------------------------
