@@ -26,7 +26,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct {
   char internal[128];
 } ncclUniqueId;
-enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclMax = 2 };
+enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 struct NcclApi {
   bool tried = false;
   void* lib = nullptr;
@@ -34,6 +34,7 @@ struct NcclApi {
   int (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*commDestroy)(ncclComm_t) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
 };
 NcclApi g_nccl;
@@ -49,8 +50,10 @@ bool nccl_load(std::string* why) {
       g_nccl.commInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
       g_nccl.allReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
       g_nccl.commDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+      g_nccl.allGather = (int (*)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllGather");
       g_nccl.getErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
-      if (g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy) g_nccl.lib = h;
+      if (g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.allGather)
+        g_nccl.lib = h;
     }
   }
   if (!g_nccl.lib && why) *why = "libnccl.so.2 not loadable";
@@ -133,7 +136,7 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 int64_t pad_jobs(int64_t n_jobs) { return (n_jobs + 63) / 64 * 64; }
 
 size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
-                        int64_t n_sets_local, char* base, Workspace* ws) {
+                        int64_t n_sets_local, int nranks, char* base, Workspace* ws) {
   size_t off = 0;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + off : nullptr;
@@ -154,6 +157,15 @@ size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_
   w.picked = (unsigned long long*)take((size_t)n_jobs * 8 + 8);
   w.alive = (int64_t*)take((size_t)n_sets_local * 8 + 8);
   w.alive2 = (int64_t*)take((size_t)n_sets_local * 8 + 8);
+  w.hist = (unsigned*)take((size_t)kHistBins * 4);
+  w.mm = (unsigned*)take(16);
+  const int64_t cap = nranks > 1 ? std::min<int64_t>(n_sets_local, (int64_t)16 << 20) : n_sets_local;
+  w.batch_cap = cap;
+  const int64_t gathered = nranks > 1 ? cap * nranks : 0;
+  w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);
+  w.gath_sorted = (unsigned long long*)take((size_t)gathered * 8 + 8);
+  w.sort_tmp_bytes = sort_temp_bytes(std::max<int64_t>(nranks > 1 ? gathered : n_sets_local, 1));
+  w.sort_tmp = take(w.sort_tmp_bytes);
   w.bytes = off;
   if (ws) *ws = w;
   return off;
@@ -421,7 +433,7 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
   if (!h || !bytes || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad workspace_size arguments");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, nullptr, nullptr);
+  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, nullptr, nullptr);
   return COSCHED_OK;
 }
 
@@ -480,8 +492,17 @@ cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks) {
   return COSCHED_OK;
 }
 
+static cosched_status allreduce_op(cosched_t h, void* dev, size_t count, int dtype, int op) {
+  if (h->nranks <= 1 || !h->comm) return COSCHED_OK;
+  int r = g_nccl.allReduce(dev, dev, count, dtype, op, h->comm, h->stream);
+  if (r != 0)
+    return fail(h, COSCHED_E_NCCL, std::string("ncclAllReduce: ") +
+                                       (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  return COSCHED_OK;
+}
+
 static cosched_status allreduce_max(cosched_t h, void* dev, size_t count, int dtype) {
-  if (h->nranks <= 1) return COSCHED_OK;
+  if (h->nranks <= 1 || !h->comm) return COSCHED_OK;
   int r = g_nccl.allReduce(dev, dev, count, dtype, kNcclMax, h->comm, h->stream);
   if (r != 0)
     return fail(h, COSCHED_E_NCCL, std::string("ncclAllReduce: ") +
@@ -501,7 +522,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     return fail(h, COSCHED_E_ARG, "queue too large: more than 2^32-2 sets");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, nullptr, nullptr);
+  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, nullptr, nullptr);
   if (!workspace_dev || workspace_bytes < need || ((uintptr_t)workspace_dev & 255))
     return fail(h, COSCHED_E_OOM, "workspace missing, misaligned or smaller than cosched_workspace_size");
   float* obj = nullptr;
@@ -515,7 +536,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   DeviceGuard g(h->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Workspace ws;
-  workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, (char*)workspace_dev, &ws);
+  workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, (char*)workspace_dev, &ws);
   h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
   launch_fill_u64(ws.err, ~0ull, 1, st);
@@ -652,6 +673,101 @@ static int64_t n_partitions(int k, int64_t n) {
   return acc;
 }
 
+
+// Sequential greedy by a sorted scan (greedy.cu). Picks come back in greedy
+// order. *fallback = true when a batch would exceed the workspace capacity.
+static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<unsigned long long>* picks,
+                                         bool* fallback) {
+  Workspace& ws = h->ws;
+  const int ns = h->n_slots;
+  const int64_t N = h->n_jobs;
+  const int W = h->comm ? h->nranks : 1;
+  *fallback = false;
+  cudaStream_t s = h->stream;
+  h->greedy_rounds = 0;
+  // 1. objective range and histogram over every rank's sets
+  unsigned init_mm[2] = {0xFFFFFFFFu, 0u};
+  CK(cudaMemcpyAsync(ws.mm, init_mm, 8, cudaMemcpyHostToDevice, s));
+  launch_obj_minmax(h->out_obj, h->n_sets, ws.mm, s);
+  h->launches++;
+  cosched_status st = allreduce_op(h, ws.mm, 1, kNcclUint32, kNcclMin);
+  if (st != COSCHED_OK) return st;
+  st = allreduce_op(h, ws.mm + 1, 1, kNcclUint32, kNcclMax);
+  if (st != COSCHED_OK) return st;
+  CK(cudaMemsetAsync(ws.hist, 0, (size_t)kHistBins * 4, s));
+  launch_obj_hist(h->out_obj, h->n_sets, ws.mm, kHistBins, ws.hist, s);
+  h->launches++;
+  st = allreduce_op(h, ws.hist, kHistBins, kNcclUint32, kNcclSum);
+  if (st != COSCHED_OK) return st;
+  std::vector<unsigned> hist(kHistBins);
+  unsigned mmh[2];
+  CK(cudaMemcpyAsync(hist.data(), ws.hist, (size_t)kHistBins * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(mmh, ws.mm, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  picks->clear();
+  if (mmh[0] > mmh[1]) return COSCHED_OK;  // no feasible set anywhere
+  // 2. batches of bins, from the top, of ~kBatch keys (global)
+  const int64_t kBatch = std::min<int64_t>(ws.batch_cap, (int64_t)8 << 20);
+  uint32_t* taken_bits = ws.taken;
+  CK(cudaMemsetAsync(taken_bits, 0, (size_t)((N + 31) / 32) * 4, s));
+  int64_t* np_dev = ws.counters + 1;
+  unsigned long long* nk_dev = (unsigned long long*)(ws.counters + 2);
+  CK(cudaMemsetAsync(np_dev, 0, 8, s));
+  int bin_hi = kHistBins - 1;
+  int64_t n_picks = 0;
+  while (bin_hi >= 0 && n_picks < k) {
+    int bin_lo = bin_hi;
+    int64_t acc = hist[bin_hi];
+    while (bin_lo > 0 && acc + hist[bin_lo - 1] <= kBatch) acc += hist[--bin_lo];
+    if (acc == 0) {
+      bin_hi = bin_lo - 1;
+      continue;
+    }
+    // 3. compact this rank's keys in the range; gather over ranks; sort; scan
+    CK(cudaMemsetAsync(nk_dev, 0, 8, s));
+    launch_keys_in_range(h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi,
+                         (unsigned long long*)ws.alive, nk_dev, s);
+    h->launches++;
+    int64_t nk = 0;
+    CK(cudaMemcpyAsync(&nk, nk_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const unsigned long long* list = (const unsigned long long*)ws.alive;
+    unsigned long long* sorted = (unsigned long long*)ws.alive2;
+    int64_t m = nk;
+    if (W > 1) {
+      int64_t mx = nk;
+      CK(cudaMemcpyAsync(ws.counters + 4, &mx, 8, cudaMemcpyHostToDevice, s));
+      st = allreduce_op(h, ws.counters + 4, 1, kNcclUint64, kNcclMax);
+      if (st != COSCHED_OK) return st;
+      CK(cudaMemcpyAsync(&mx, ws.counters + 4, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (mx > ws.batch_cap) {
+        *fallback = true;
+        return COSCHED_OK;
+      }
+      if (mx > nk) CK(cudaMemsetAsync((unsigned long long*)ws.alive + nk, 0, (size_t)(mx - nk) * 8, s));
+      int r = g_nccl.allGather(ws.alive, ws.gath, (size_t)mx, kNcclUint64, h->comm, s);
+      if (r != 0) return fail(h, COSCHED_E_NCCL, "ncclAllGather failed");
+      list = ws.gath;
+      sorted = ws.gath_sorted;
+      m = mx * W;
+    }
+    CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s));
+    CK(launch_greedy_scan(ns, sorted, m, N, taken_bits, ws.picked, np_dev, k, s));
+    h->launches += 2;
+    h->greedy_rounds++;
+    CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bin_hi = bin_lo - 1;
+  }
+  picks->resize(n_picks);
+  if (n_picks) {
+    CK(cudaMemcpyAsync(picks->data(), ws.picked, (size_t)n_picks * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return COSCHED_OK;
+}
+
 cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids, int32_t* cfgs, double* total_obj,
                                        int32_t* n_found) {
   if (!h || k < 1 || !set_ids) return fail(h, COSCHED_E_ARG, "bad allocation arguments");
@@ -693,8 +809,36 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     if (n_found) *n_found = k;
     return COSCHED_OK;
   }
-  // greedy: locally dominant rounds over this rank's shard
+  // greedy: sorted scan (greedy.cu); locally-dominant rounds only as a fallback
   if (!h->out_obj) return fail(h, COSCHED_E_STATE, "greedy allocation needs score_all with out->obj");
+  {
+    std::vector<unsigned long long> picks;
+    bool fallback = false;
+    st = greedy_sorted_scan(h, k, &picks, &fallback);
+    if (st != COSCHED_OK) return st;
+    if (!fallback) {
+      if (picks.empty()) return COSCHED_INFEASIBLE;
+      int64_t take = std::min<int64_t>(k, (int64_t)picks.size());
+      std::vector<int64_t> ids(take);
+      double tot = 0.0;
+      for (int64_t i = 0; i < take; i++) {
+        float o;
+        cosched_unpack_key(picks[i], &o, &ids[i]);
+        set_ids[i] = ids[i];
+        tot += (double)o;
+      }
+      if (cfgs) {
+        std::vector<float> rows;
+        st = detail_rows(h, ids.data(), take, &rows);
+        if (st != COSCHED_OK) return st;
+        for (int64_t i = 0; i < take; i++) memcpy(&cfgs[i], &rows[i * 8], 4);
+      }
+      if (total_obj) *total_obj = tot;
+      if (n_found) *n_found = (int32_t)take;
+      return COSCHED_OK;
+    }
+  }
+  // fallback: locally dominant rounds over this rank's shard
   Workspace& ws = h->ws;
   int64_t* cnt = ws.counters;  // [0] n_alive, [1] n_picked, [2] n_alive2
   launch_fill_u64((unsigned long long*)cnt, 0ull, 8, h->stream);

@@ -61,11 +61,30 @@ struct Workspace {
   int64_t* alive2 = nullptr;               // [n_sets_local]
   unsigned long long* picked = nullptr;    // [n_jobs] greedy picked keys
   int64_t* counters = nullptr;             // [8] device counters
+  unsigned* hist = nullptr;                // [kHistBins] greedy objective histogram
+  unsigned* mm = nullptr;                  // [2] min / max ord(obj)
+  unsigned long long* gath = nullptr;      // [nranks * batch_cap] gathered keys (multi-rank)
+  unsigned long long* gath_sorted = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  int64_t batch_cap = 0;                   // keys per rank per greedy batch
   size_t bytes = 0;
 };
 
+constexpr int kHistBins = 65536;
 size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
-                        int64_t n_sets_local, char* base, Workspace* ws);
+                        int64_t n_sets_local, int nranks, char* base, Workspace* ws);
+// greedy.cu
+void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st);
+void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st);
+void launch_keys_in_range(const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins, int bin_lo,
+                          int bin_hi, unsigned long long* keys, unsigned long long* n_keys, cudaStream_t st);
+size_t sort_temp_bytes(int64_t n);
+cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
+                           int64_t n, cudaStream_t st);
+cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
+                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
+                               cudaStream_t st);
 int64_t pad_jobs(int64_t n_jobs);
 
 // ---- kernel launchers (defined in kernels.cu) ------------------------------------

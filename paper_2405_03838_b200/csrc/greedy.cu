@@ -1,0 +1,193 @@
+// greedy.cu -- job -> GPU allocation by the sequential greedy rule (DESIGN.md
+// R12): repeatedly take the feasible set with the largest (objective, -id)
+// whose jobs are all free. Exactly that order is reproduced on the GPU:
+//
+//   1. histogram of ord(obj) over the feasible sets (64 K bins between the
+//      queue's min and max objective) -> descending key ranges ("batches") of
+//      ~M keys each;
+//   2. per batch: compact the packed keys (ord(obj) << 32 | ~id) of the range,
+//      radix-sort them descending (CUB), and
+//   3. scan them in order with one resident block: 1024 keys at a time every
+//      thread decodes its set and tests its jobs against the taken bitmask in
+//      shared memory (parallel filter); one warp then walks the surviving
+//      candidates in order and takes each one still free (the sequential rule).
+//      The scan stops at k picks; otherwise the next batch continues it.
+//
+// Multi-GPU: batch ranges come from the all-reduced histogram, each rank's
+// compacted keys are all-gathered, so every rank sorts and scans the same list
+// and returns identical picks.
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "cosched_internal.h"
+#include "device_common.cuh"
+
+namespace cosched {
+
+__global__ void k_obj_minmax(const float* __restrict__ obj, int64_t count, unsigned* mm /* [0] min ord, [1] max ord */) {
+  unsigned lo = 0xFFFFFFFFu, hi = 0u;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+    float o = obj[k];
+    if (o > -INFINITY) {
+      unsigned u = ord_float_d(o);
+      lo = u < lo ? u : lo;
+      hi = u > hi ? u : hi;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo, off), b = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lo != 0xFFFFFFFFu) atomicMin(&mm[0], lo);
+    if (hi) atomicMax(&mm[1], hi);
+  }
+}
+
+__device__ __forceinline__ int bin_of(unsigned u, unsigned lo, unsigned span, int nbins) {
+  return (int)(((unsigned long long)(u - lo) * (unsigned long long)nbins) / ((unsigned long long)span + 1ull));
+}
+
+__global__ void k_obj_hist(const float* __restrict__ obj, int64_t count, const unsigned* __restrict__ mm, int nbins,
+                           unsigned* hist) {
+  const unsigned lo = mm[0], span = mm[1] - mm[0];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+    float o = obj[k];
+    if (o > -INFINITY) atomicAdd(&hist[bin_of(ord_float_d(o), lo, span, nbins)], 1u);
+  }
+}
+
+// keys of the sets whose bin lies in [bin_lo, bin_hi]
+__global__ void k_keys_in_range(const float* __restrict__ obj, int64_t first, int64_t count,
+                                const unsigned* __restrict__ mm, int nbins, int bin_lo, int bin_hi,
+                                unsigned long long* keys, unsigned long long* n_keys) {
+  const unsigned lo = mm[0], span = mm[1] - mm[0];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+    float o = obj[k];
+    if (!(o > -INFINITY)) continue;
+    int b = bin_of(ord_float_d(o), lo, span, nbins);
+    if (b < bin_lo || b > bin_hi) continue;
+    unsigned long long at = atomicAdd(n_keys, 1ull);
+    keys[at] = pack_key(o, first + k);
+  }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(1024, 1)
+    k_greedy_scan(const unsigned long long* __restrict__ sorted, int64_t m, int64_t n_jobs, uint32_t* taken_g,
+                  unsigned long long* picks, int64_t* n_picks, int64_t k_max) {
+  extern __shared__ uint32_t s_taken[];  // n_jobs bits
+  __shared__ int32_t s_job[1024][NS];
+  __shared__ uint32_t s_flag[32];
+  __shared__ int64_t s_np;
+  const int words = (int)((n_jobs + 31) >> 5);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) s_taken[i] = taken_g[i];
+  if (threadIdx.x == 0) s_np = *n_picks;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += 1024) {
+    if (s_np >= k_max) break;
+    const int64_t i = base + threadIdx.x;
+    bool fr = false;
+    if (i < m) {
+      const unsigned long long key = sorted[i];
+      if (key) {
+        const int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+        int64_t j[3];
+        unrank_set<NS>(sid, j);
+        fr = true;
+#pragma unroll
+        for (int q = 0; q < NS; q++) {
+          s_job[threadIdx.x][q] = (int32_t)j[q];
+          fr = fr && !((s_taken[j[q] >> 5] >> (j[q] & 31)) & 1u);
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, fr);
+    if ((threadIdx.x & 31) == 0) s_flag[threadIdx.x >> 5] = bal;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // one warp applies the sequential rule to the window's free candidates, in order
+      int64_t np = s_np;
+      for (int w = 0; w < 32 && np < k_max; w++) {
+        unsigned mask = s_flag[w];
+        while (mask && np < k_max) {
+          const int b = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int t = w * 32 + b;
+          bool ok = true;
+#pragma unroll
+          for (int q = 0; q < NS; q++) {
+            const int jj = s_job[t][q];
+            ok = ok && !((s_taken[jj >> 5] >> (jj & 31)) & 1u);
+          }
+          if (ok) {
+            __syncwarp();
+            if (threadIdx.x == 0) {
+#pragma unroll
+              for (int q = 0; q < NS; q++) {
+                const int jj = s_job[t][q];
+                s_taken[jj >> 5] |= 1u << (jj & 31);
+              }
+              picks[np] = sorted[base + t];
+            }
+            __syncwarp();
+            np++;
+          }
+        }
+      }
+      if (threadIdx.x == 0) s_np = np;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < words; i += blockDim.x) taken_g[i] = s_taken[i];
+  if (threadIdx.x == 0) *n_picks = s_np;
+}
+
+// ---- launchers -------------------------------------------------------------------------
+void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st) {
+  if (count <= 0) return;
+  int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  k_obj_minmax<<<(unsigned)blocks, 256, 0, st>>>(obj, count, mm);
+}
+void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st) {
+  if (count <= 0) return;
+  int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  k_obj_hist<<<(unsigned)blocks, 256, 0, st>>>(obj, count, mm, nbins, hist);
+}
+void launch_keys_in_range(const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins, int bin_lo,
+                          int bin_hi, unsigned long long* keys, unsigned long long* n_keys, cudaStream_t st) {
+  if (count <= 0) return;
+  int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  k_keys_in_range<<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, keys, n_keys);
+}
+
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeysDescending((void*)nullptr, bytes, (const unsigned long long*)nullptr,
+                                           (unsigned long long*)nullptr, (int)std::max<int64_t>(n, 1));
+  return bytes;
+}
+
+cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
+                           int64_t n, cudaStream_t st) {
+  return cub::DeviceRadixSort::SortKeysDescending(temp, temp_bytes, in, out, (int)n, 0, 64, st);
+}
+
+cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
+                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
+                               cudaStream_t st) {
+  const size_t smem = (size_t)((n_jobs + 31) / 32) * 4;
+  if (n_slots == 2) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_greedy_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_greedy_scan<2><<<1, 1024, smem, st>>>(sorted, m, n_jobs, taken_bits, picks, n_picks, k_max);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_greedy_scan<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_greedy_scan<3><<<1, 1024, smem, st>>>(sorted, m, n_jobs, taken_bits, picks, n_picks, k_max);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cosched

@@ -39,7 +39,7 @@ namespace {
 constexpr int kTile = 64;      // pairs per tile side
 constexpr int kThreads = 256;  // 16 x 16 threads, 4 x 4 pairs each
 constexpr int kM = 4;          // micro-tile side
-constexpr int kBgRow = kTile + 1;
+constexpr int kBgRow = kTile + 4;  // (4*ty + tx) mod 32: the group-end LDS/STS of a warp hit distinct banks
 
 __device__ __forceinline__ float min3f(float a, float b, float c) {
   float r;
@@ -139,7 +139,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int kRS = NP ? (((NP >> 2) & 1) ? NP : NP + 4) : 0;
   const int rs = NP ? kRS : sp.rs;
   const int stage_floats = 6 * kTile * rs;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // thread -> (tx, ty): a warp covers 4 j0 rows x 8 j1 rows, so each float4
+  // operand load is one 128-byte shared-memory wavefront (j0 rows broadcast to
+  // 8 lanes, 8 consecutive j1 rows in distinct bank groups)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = ((warp & 3) << 2) | (lane & 3), ty = ((warp >> 2) << 3) | (lane >> 2);
   const int rs4 = rs >> 2;
   const int gps = NP ? (NP >> 2) / G : g.groups_per_state;
   unsigned long long key = 0;
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     sbest[e] = 0.0f;  // feasible masked objectives are > 0
     sbg[e] = -1;
   }
+  __syncthreads();  // the owners of each pair read these at their first group end
 
   while (true) {
     // prefetch the next (tile, state) into the other buffer

@@ -277,3 +277,15 @@ def test_c5_triples_sampled(cs):
     assert not fails, fails[:5]
     st, sid, cfg, ob = s.best_set()
     assert st == 0 and ob == obj_g.max()
+
+
+@pytest.mark.parametrize("k", [1, 37, 60])
+def test_greedy_partial_and_ties(cs, k):
+    pb = make_problem("b200", "c21", coef_seed=16, alpha=0.3, mirror_ties=True)
+    F = tie_stress_features(120, seed=16, frac=0.25)
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    st, ids, cfgs, tot = s.best_allocation(k)
+    assert st == 0 and len(ids) == k
+    _, obj_o = Oracle(pb).score_range(F)
+    ok, why = replay_greedy(120, 2, obj_o, ids)
+    assert ok, why
