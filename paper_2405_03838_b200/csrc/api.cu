@@ -164,7 +164,8 @@ size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_
   const int64_t gathered = nranks > 1 ? cap * nranks : 0;
   w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);
   w.gath_sorted = (unsigned long long*)take((size_t)gathered * 8 + 8);
-  w.sort_tmp_bytes = sort_temp_bytes(std::max<int64_t>(nranks > 1 ? gathered : n_sets_local, 1));
+  const int64_t list_max = std::max<int64_t>(nranks > 1 ? gathered : n_sets_local, 1);
+  w.sort_tmp_bytes = std::max(sort_temp_bytes(list_max), select_temp_bytes(list_max));
   w.sort_tmp = take(w.sort_tmp_bytes);
   w.bytes = off;
   if (ws) *ws = w;
@@ -707,7 +708,9 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   picks->clear();
   if (mmh[0] > mmh[1]) return COSCHED_OK;  // no feasible set anywhere
   // 2. batches of bins, from the top, of ~kBatch keys (global)
-  const int64_t kBatch = std::min<int64_t>(ws.batch_cap, (int64_t)8 << 20);
+  // a batch is a range of objective bins holding ~kBatch feasible sets; only the
+  // sets whose jobs are all still free are compacted and sorted
+  const int64_t kBatch = std::min<int64_t>(ws.batch_cap, (int64_t)64 << 20);
   uint32_t* taken_bits = ws.taken;
   CK(cudaMemsetAsync(taken_bits, 0, (size_t)((N + 31) / 32) * 4, s));
   int64_t* np_dev = ws.counters + 1;
@@ -725,7 +728,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     }
     // 3. compact this rank's keys in the range; gather over ranks; sort; scan
     CK(cudaMemsetAsync(nk_dev, 0, 8, s));
-    launch_keys_in_range(h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi,
+    launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
                          (unsigned long long*)ws.alive, nk_dev, s);
     h->launches++;
     int64_t nk = 0;
@@ -753,11 +756,29 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       m = mx * W;
     }
     CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s));
-    CK(launch_greedy_scan(ns, sorted, m, N, taken_bits, ws.picked, np_dev, k, s));
-    h->launches += 2;
-    h->greedy_rounds++;
-    CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    h->launches++;
+    // scan the sorted list in chunks; between chunks drop (order-preserving)
+    // every key whose set touches a job taken meanwhile
+    unsigned long long* cur = sorted;
+    unsigned long long* spare = (W > 1) ? ws.gath : (unsigned long long*)ws.alive;
+    const int64_t kChunk = 1 << 16;
+    while (m > 0 && n_picks < k) {
+      const int64_t len = std::min<int64_t>(m, kChunk);
+      CK(launch_greedy_scan(ns, cur, len, N, taken_bits, ws.picked, np_dev, k, s));
+      h->launches++;
+      h->greedy_rounds++;
+      CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
+      if (m > len) {
+        CK(select_free_keys(ns, ws.sort_tmp, ws.sort_tmp_bytes, cur + len, spare, ws.counters + 3, m - len, taken_bits,
+                            s));
+        h->launches++;
+        CK(cudaMemcpyAsync(&m, ws.counters + 3, 8, cudaMemcpyDeviceToHost, s));
+        std::swap(cur, spare);
+      } else {
+        m = 0;
+      }
+      CK(cudaStreamSynchronize(s));
+    }
     bin_hi = bin_lo - 1;
   }
   picks->resize(n_picks);

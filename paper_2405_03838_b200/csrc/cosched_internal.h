@@ -77,9 +77,14 @@ size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_
 // greedy.cu
 void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st);
 void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st);
-void launch_keys_in_range(const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins, int bin_lo,
-                          int bin_hi, unsigned long long* keys, unsigned long long* n_keys, cudaStream_t st);
+void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
+                          int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
+                          unsigned long long* n_keys, cudaStream_t st);
 size_t sort_temp_bytes(int64_t n);
+size_t select_temp_bytes(int64_t n);
+cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const unsigned long long* in,
+                             unsigned long long* out, int64_t* n_out, int64_t n, const uint32_t* taken_bits,
+                             cudaStream_t st);
 cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
                            int64_t n, cudaStream_t st);
 cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,

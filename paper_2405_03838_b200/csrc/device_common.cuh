@@ -33,6 +33,33 @@ __device__ __forceinline__ const float* w_row(const float* __restrict__ base, co
   return base + (((int64_t)slot * sp.n_states + state) * sp.n_jobs_pad + job) * sp.rs;
 }
 
+// One candidate (set j[], state s, cap p) in the canonical FP32 evaluation
+// order shared by every scorer (generic, tiled pairs, tiled triples, detail):
+//   pairs:   r0 = ka0 + kb1,              r1 = ka1 + kb0,              o = w0 + w1
+//   triples: r0 = ka0 + (kb1 + kb2),      r1 = (ka1 + kb2) + kb0,
+//            r2 = (ka2 + kb1) + kb0,      o  = w0 + (w1 + w2)
+// (kaX = ka[s_slot][j_X], kbX = kb[s_slot][j_X] for the slot being scored.)
+template <int NS, typename SP>
+__device__ __forceinline__ void eval_cfg(const SP& sp, const float* __restrict__ ka, const float* __restrict__ kb,
+                                         const float* __restrict__ w, const int64_t* j, int s, int p, float* r,
+                                         float* o) {
+  if (NS == 1) {
+    r[0] = ka_row(ka, sp, sp.slice[s][0], j[0])[p];
+    *o = w_row(w, sp, 0, s, j[0])[p];
+  } else if (NS == 2) {
+    const int s0 = sp.slice[s][0], s1 = sp.slice[s][1];
+    r[0] = __fadd_rn(ka_row(ka, sp, s0, j[0])[p], ka_row(kb, sp, s0, j[1])[p]);
+    r[1] = __fadd_rn(ka_row(ka, sp, s1, j[1])[p], ka_row(kb, sp, s1, j[0])[p]);
+    *o = __fadd_rn(w_row(w, sp, 0, s, j[0])[p], w_row(w, sp, 1, s, j[1])[p]);
+  } else {
+    const int s0 = sp.slice[s][0], s1 = sp.slice[s][1], s2 = sp.slice[s][2];
+    r[0] = __fadd_rn(ka_row(ka, sp, s0, j[0])[p], __fadd_rn(ka_row(kb, sp, s0, j[1])[p], ka_row(kb, sp, s0, j[2])[p]));
+    r[1] = __fadd_rn(__fadd_rn(ka_row(ka, sp, s1, j[1])[p], ka_row(kb, sp, s1, j[2])[p]), ka_row(kb, sp, s1, j[0])[p]);
+    r[2] = __fadd_rn(__fadd_rn(ka_row(ka, sp, s2, j[2])[p], ka_row(kb, sp, s2, j[1])[p]), ka_row(kb, sp, s2, j[0])[p]);
+    *o = __fadd_rn(w_row(w, sp, 0, s, j[0])[p], __fadd_rn(w_row(w, sp, 1, s, j[1])[p], w_row(w, sp, 2, s, j[2])[p]));
+  }
+}
+
 // order-preserving float -> u32 (larger float <=> larger u32; -0 < +0)
 __device__ __forceinline__ uint32_t ord_float_d(float f) {
   uint32_t b = __float_as_uint(f);

@@ -17,6 +17,7 @@
 // compacted keys are all-gathered, so every rank sorts and scans the same list
 // and returns identical picks.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -60,16 +61,25 @@ __global__ void k_obj_hist(const float* __restrict__ obj, int64_t count, const u
   }
 }
 
-// keys of the sets whose bin lies in [bin_lo, bin_hi]
+// keys of the sets whose bin lies in [bin_lo, bin_hi] and whose jobs are all
+// still free (sets touching a taken job can never be picked again)
+template <int NS>
 __global__ void k_keys_in_range(const float* __restrict__ obj, int64_t first, int64_t count,
                                 const unsigned* __restrict__ mm, int nbins, int bin_lo, int bin_hi,
-                                unsigned long long* keys, unsigned long long* n_keys) {
+                                const uint32_t* __restrict__ taken_bits, unsigned long long* keys,
+                                unsigned long long* n_keys) {
   const unsigned lo = mm[0], span = mm[1] - mm[0];
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
     float o = obj[k];
     if (!(o > -INFINITY)) continue;
     int b = bin_of(ord_float_d(o), lo, span, nbins);
     if (b < bin_lo || b > bin_hi) continue;
+    int64_t j[3];
+    unrank_set<NS>(first + k, j);
+    bool fr = true;
+#pragma unroll
+    for (int q = 0; q < NS; q++) fr = fr && !((__ldg(taken_bits + (j[q] >> 5)) >> (j[q] & 31)) & 1u);
+    if (!fr) continue;
     unsigned long long at = atomicAdd(n_keys, 1ull);
     keys[at] = pack_key(o, first + k);
   }
@@ -146,6 +156,42 @@ __global__ void __launch_bounds__(1024, 1)
   if (threadIdx.x == 0) *n_picks = s_np;
 }
 
+// predicate of the order-preserving re-filter between scan chunks
+template <int NS>
+struct AllJobsFree {
+  const uint32_t* bits;
+  __device__ __forceinline__ bool operator()(const unsigned long long& key) const {
+    if (!key) return false;
+    const int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+    int64_t j[3];
+    unrank_set<NS>(sid, j);
+    bool fr = true;
+#pragma unroll
+    for (int q = 0; q < NS; q++) fr = fr && !((bits[j[q] >> 5] >> (j[q] & 31)) & 1u);
+    return fr;
+  }
+};
+
+size_t select_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  AllJobsFree<2> pred{nullptr};
+  cub::DeviceSelect::If((void*)nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                        (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), pred);
+  size_t b3 = 0;
+  AllJobsFree<3> pred3{nullptr};
+  cub::DeviceSelect::If((void*)nullptr, b3, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                        (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), pred3);
+  return std::max(bytes, b3);
+}
+
+cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const unsigned long long* in,
+                             unsigned long long* out, int64_t* n_out, int64_t n, const uint32_t* taken_bits,
+                             cudaStream_t st) {
+  if (n_slots == 2)
+    return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<2>{taken_bits}, st);
+  return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<3>{taken_bits}, st);
+}
+
 // ---- launchers -------------------------------------------------------------------------
 void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st) {
   if (count <= 0) return;
@@ -157,11 +203,17 @@ void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nb
   int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
   k_obj_hist<<<(unsigned)blocks, 256, 0, st>>>(obj, count, mm, nbins, hist);
 }
-void launch_keys_in_range(const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins, int bin_lo,
-                          int bin_hi, unsigned long long* keys, unsigned long long* n_keys, cudaStream_t st) {
+void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
+                          int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
+                          unsigned long long* n_keys, cudaStream_t st) {
   if (count <= 0) return;
   int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
-  k_keys_in_range<<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, keys, n_keys);
+  if (n_slots == 2)
+    k_keys_in_range<2><<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, taken_bits,
+                                                          keys, n_keys);
+  else
+    k_keys_in_range<3><<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, taken_bits,
+                                                          keys, n_keys);
 }
 
 size_t sort_temp_bytes(int64_t n) {

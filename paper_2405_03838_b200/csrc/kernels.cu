@@ -167,29 +167,12 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
     float best = -INFINITY;
     int32_t bc = -1;
     for (int s = 0; s < sp.n_states; s++) {
-      const float* a[NS];
-      const float* b[NS][NS];
-      const float* ww[NS];
-#pragma unroll
-      for (int i = 0; i < NS; i++) {
-        int sl = sp.slice[s][i];
-        a[i] = ka_row(ka, sp, sl, j[i]);
-        ww[i] = w_row(w, sp, i, s, j[i]);
-#pragma unroll
-        for (int l = 0; l < NS; l++) b[i][l] = ka_row(kb, sp, sl, j[l]);
-      }
       for (int p = 0; p < sp.n_caps; p++) {
-        float o = 0.0f;
+        float r[NS], o;
+        eval_cfg<NS>(sp, ka, kb, w, j, s, p, r, &o);
         bool feas = true;
 #pragma unroll
-        for (int i = 0; i < NS; i++) {
-          float r = a[i][p];
-#pragma unroll
-          for (int l = 0; l < NS; l++)
-            if (l != i) r = __fadd_rn(r, b[i][l][p]);
-          feas = feas && (r > 0.0f);
-          o = (i == 0) ? ww[i][p] : __fadd_rn(o, ww[i][p]);
-        }
+        for (int i = 0; i < NS; i++) feas = feas && (r[i] > 0.0f);
         if (feas && o > best) {
           best = o;
           bc = s * sp.n_caps + p;
@@ -207,12 +190,18 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
                             int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                             const unsigned long long* err, cudaStream_t st);
 
+int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
+                              int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                              const unsigned long long* err, cudaStream_t st);
+
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                  const unsigned long long* err, int variant, cudaStream_t st) {
   if (count <= 0) return 0;
   if (variant != 0 && sp.n_slots == 2)
     return launch_score_pairs_fast(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, st);
+  if (variant != 0 && sp.n_slots == 3)
+    return launch_score_triples_fast(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, st);
   int bs = 256;
   unsigned grid = (unsigned)((count + bs - 1) / bs);
   if (sp.n_slots == 1)
@@ -242,17 +231,12 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
   unsigned long long key = 0;
   for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
     int s = c / sp.n_caps, p = c % sp.n_caps;
-    float u = 0.0f;
+    float r[3], u;
+    if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, &u);
+    else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, &u);
+    else eval_cfg<3>(sp, ka, kb, w, j, s, p, r, &u);
     bool feas = true;
-    for (int i = 0; i < sp.n_slots; i++) {
-      int sl = sp.slice[s][i];
-      float r = ka_row(ka, sp, sl, j[i])[p];
-      for (int l = 0; l < sp.n_slots; l++)
-        if (l != i) r = __fadd_rn(r, ka_row(kb, sp, sl, j[l])[p]);
-      feas = feas && (r > 0.0f);
-      float wi = w_row(w, sp, i, s, j[i])[p];
-      u = (i == 0) ? wi : __fadd_rn(u, wi);
-    }
+    for (int i = 0; i < sp.n_slots; i++) feas = feas && (r[i] > 0.0f);
     unsigned long long kk = feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
     key = kk > key ? kk : key;
   }
@@ -270,15 +254,12 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
     }
     int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
     int s = c / sp.n_caps, p = c % sp.n_caps;
-    float thr = 0.0f, fair = INFINITY, u = 0.0f;
+    float thr = 0.0f, fair = INFINITY, u, r[3];
+    if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, &u);
+    else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, &u);
+    else eval_cfg<3>(sp, ka, kb, w, j, s, p, r, &u);
     for (int i = 0; i < sp.n_slots; i++) {
-      int sl = sp.slice[s][i];
-      float r = ka_row(ka, sp, sl, j[i])[p];
-      for (int l = 0; l < sp.n_slots; l++)
-        if (l != i) r = __fadd_rn(r, ka_row(kb, sp, sl, j[l])[p]);
-      float wi = w_row(w, sp, i, s, j[i])[p];
-      u = (i == 0) ? wi : __fadd_rn(u, wi);
-      float rp = __fmaf_rn(r, kInvScale, sp.alpha);
+      float rp = __fmaf_rn(r[i], kInvScale, sp.alpha);
       out[4 + i] = rp;
       thr = (i == 0) ? rp : __fadd_rn(thr, rp);
       fair = fminf(fair, rp);

@@ -31,6 +31,7 @@
 
 #include "cosched_internal.h"
 #include "device_common.cuh"
+#include "tile_common.cuh"
 
 namespace cosched {
 
@@ -40,50 +41,6 @@ constexpr int kTile = 64;      // pairs per tile side
 constexpr int kThreads = 256;  // 16 x 16 threads, 4 x 4 pairs each
 constexpr int kM = 4;          // micro-tile side
 constexpr int kBgRow = kTile + 4;  // (4*ty + tx) mod 32: the group-end LDS/STS of a warp hit distinct banks
-
-__device__ __forceinline__ float min3f(float a, float b, float c) {
-  float r;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-__device__ __forceinline__ float max3f(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-__device__ __forceinline__ float4 add4(float4 a, float4 b) {
-  float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
-  float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
-  return make_float4(lo.x, lo.y, hi.x, hi.y);
-}
-
-// ---- mbarrier + TMA bulk copy (PTX, sm_90+) ---------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 struct PairGrid {
   int64_t n_jobs;
@@ -257,12 +214,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int rj = e >> 6, ri = e & 63;
         const int64_t j0 = I * kTile + ri;
         const int64_t j1 = J * kTile + rj;
+        const int gb = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
+        sbg[rj * kBgRow + ri] = -1;
+        sbest[rj * kBgRow + ri] = 0.0f;
         if (!(j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1)) continue;
         float bo = -INFINITY;
         int bc = -1;
-        const int gb = sbg[rj * kBgRow + ri];
-        sbg[rj * kBgRow + ri] = -1;
-        sbest[rj * kBgRow + ri] = 0.0f;
         if (gb >= 0) {
           const int sg = gb >> 4;
           const int q0 = (gb & 15) * G;
