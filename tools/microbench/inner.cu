@@ -1,0 +1,79 @@
+// Microbenchmark: the pair scorer's inner-loop instruction mix (FADD2 x6,
+// FMNMX3 x6 per pair per 4 caps, 4x4 pairs per thread) from registers only,
+// at several warps/SM, to separate the loop's own issue limit from the
+// shared-memory / synchronisation overheads of the real kernel.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r; asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c)); return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r; asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c)); return r;
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+template <int MI, int MJ, int MINB>
+__global__ void __launch_bounds__(256, MINB) kinner(const float4* __restrict__ in, float* out, int iters) {
+  float4 a0[MI], b0[MI], w0[MI], a1[MJ], b1[MJ], w1[MJ];
+  for (int i = 0; i < MI; i++) { a0[i] = in[threadIdx.x % 7 + i]; b0[i] = in[i + 1]; w0[i] = in[i + 2]; }
+  for (int i = 0; i < MJ; i++) { a1[i] = in[i + 3]; b1[i] = in[i + 4]; w1[i] = in[threadIdx.x % 5 + i]; }
+  float m[MI][MJ];
+  for (int a = 0; a < MI; a++) for (int b = 0; b < MJ; b++) m[a][b] = 0.f;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int a = 0; a < MI; a++) {
+#pragma unroll
+      for (int b = 0; b < MJ; b++) {
+        const float4 r0 = add4(a0[a], b1[b]);
+        const float4 r1 = add4(a1[b], b0[a]);
+        const float4 o = add4(w0[a], w1[b]);
+        const float x0 = min3f(o.x, r0.x, r1.x), x1 = min3f(o.y, r0.y, r1.y);
+        const float x2 = min3f(o.z, r0.z, r1.z), x3 = min3f(o.w, r0.w, r1.w);
+        m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
+      }
+    }
+    // perturb operands so nothing is loop-invariant (1 FADD2 per row/col per iteration)
+#pragma unroll
+    for (int a = 0; a < MI; a++) a0[a] = add4(a0[a], w0[a]);
+#pragma unroll
+    for (int b = 0; b < MJ; b++) b1[b] = add4(b1[b], w1[b]);
+  }
+  float s = 0;
+  for (int a = 0; a < MI; a++) for (int b = 0; b < MJ; b++) s += m[a][b];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <int MI, int MJ, int MINB>
+void run(int warps_per_sm, int nsm, const float4* in, float* out) {
+  int threads = 256;
+  int blocks = nsm * warps_per_sm * 32 / threads;
+  int iters = 2000;
+  kinner<MI, MJ, MINB><<<blocks, threads>>>(in, out, 10);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kinner<MI, MJ, MINB><<<blocks, threads>>>(in, out, iters);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double cands = (double)blocks * threads * iters * MI * MJ * 4;
+  printf("MI=%d MJ=%d minB=%d warps/SM=%2d: %.3f ms, %.3g cand/s, %.1f cand/clk/SM @1.9GHz\n", MI, MJ, MINB, warps_per_sm, ms,
+         cands / (ms * 1e-3), cands / (ms * 1e-3) / nsm / 1.9e9);
+}
+
+int main() {
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  float4* in; float* out;
+  cudaMalloc(&in, 64 * sizeof(float4)); cudaMemset(in, 0, 64 * sizeof(float4));
+  cudaMalloc(&out, 148 * 2048 * 4 * 4);
+  run<4, 4, 1>(8, nsm, in, out);
+  run<4, 4, 2>(16, nsm, in, out);
+  run<4, 4, 2>(32, nsm, in, out);
+  run<4, 8, 1>(8, nsm, in, out);
+  run<2, 4, 4>(32, nsm, in, out);
+  run<2, 4, 2>(16, nsm, in, out);
+  return 0;
+}
