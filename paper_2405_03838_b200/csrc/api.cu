@@ -135,8 +135,9 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int64_t pad_jobs(int64_t n_jobs) { return (n_jobs + 63) / 64 * 64; }
 
-size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
-                        int64_t n_sets_local, int nranks, char* base, Workspace* ws) {
+size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_local, int nranks, char* base,
+                        Workspace* ws) {
+  const int32_t n_slices = sp.n_slices, rs = sp.rs, n_slots = sp.n_slots, n_states = sp.n_states;
   size_t off = 0;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + off : nullptr;
@@ -149,6 +150,8 @@ size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_
   w.ka = (float*)take(proj);
   w.kb = (float*)take(proj);
   w.w = (float*)take(jp * n_slots * n_states * rs * sizeof(float));
+  w.fast = (float*)take(jp * sp.n_roles * sp.n_stages * kStageRS * sizeof(float));
+  w.wmm = (unsigned*)take(2 * kMaxSlots * sizeof(unsigned));
   w.best_key = (unsigned long long*)take(8);
   w.err = (unsigned long long*)take(8);
   w.counters = (int64_t*)take(8 * 8);
@@ -293,7 +296,10 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
   sp.np = (d->n_caps + 3) & ~3;
   sp.rs = ((sp.np >> 2) & 1) ? sp.np : sp.np + 4;
   sp.n_jobs_pad = 0;
+
   sp.n_cfg = d->n_states * d->n_caps;
+  sp.n_stages = (sp.n_cfg + kStageCfg - 1) / kStageCfg;
+  sp.n_roles = sp.n_slots * (sp.n_slots + 1);
   sp.alpha = d->alpha;
   for (int p = 0; p < d->n_caps; p++) {
     float inv = d->objective == 2 ? 1.0f / d->caps_w[p] : 1.0f;
@@ -434,7 +440,7 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
   if (!h || !bytes || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad workspace_size arguments");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  *bytes = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, nullptr, nullptr);
+  *bytes = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, nullptr, nullptr);
   return COSCHED_OK;
 }
 
@@ -523,7 +529,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     return fail(h, COSCHED_E_ARG, "queue too large: more than 2^32-2 sets");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  size_t need = workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, nullptr, nullptr);
+  size_t need = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, nullptr, nullptr);
   if (!workspace_dev || workspace_bytes < need || ((uintptr_t)workspace_dev & 255))
     return fail(h, COSCHED_E_OOM, "workspace missing, misaligned or smaller than cosched_workspace_size");
   float* obj = nullptr;
@@ -537,7 +543,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   DeviceGuard g(h->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Workspace ws;
-  workspace_layout(n_jobs, h->sp.n_slices, h->sp.rs, h->sp.n_slots, h->sp.n_states, count, h->comm ? h->nranks : 1, (char*)workspace_dev, &ws);
+  workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, (char*)workspace_dev, &ws);
   h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
   launch_fill_u64(ws.err, ~0ull, 1, st);
@@ -545,11 +551,11 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   h->launches += 2;
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, st);
-    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, st);
-    h->launches += 2;
+    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
+    h->launches += 5;
   }
   cudaEventRecord(h->ev[1], st);
-  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
+  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
   cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
@@ -806,7 +812,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     // score every set of the (tiny) queue locally: no collective needed
     int64_t all = cosched::n_sets(N, ns);
     launch_fill_u64(h->d_small_key, 0ull, 2, h->stream);
-    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, 0, all, h->d_small_obj, h->d_small_cfg,
+    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, h->ws.fast, 0, all, h->d_small_obj, h->d_small_cfg,
                                     h->d_small_key, h->ws.err, h->variant, h->stream);
     int64_t nm = n_partitions(ns, N);
     launch_exact_alloc(ns, N, h->d_small_obj, nm, h->d_small_key + 1, h->stream);

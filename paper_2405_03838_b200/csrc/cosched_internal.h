@@ -15,6 +15,11 @@ constexpr int kMaxCaps = 64;
 constexpr int kMaxStates = 128;
 constexpr int kMaxSlices = 128;
 constexpr int kMaxSlots = 3;
+// The tiled scorers walk the flattened config space c = state * n_caps + cap in
+// stages of kStageCfg consecutive configs; each stage row is padded to kStageRS
+// floats (7 float4: odd, so 8 consecutive rows hit distinct shared-memory bank groups).
+constexpr int kStageCfg = 24;
+constexpr int kStageRS = 28;
 
 // Feasibility scale: the projection stores
 // K*(U - alpha) and K*V, so a slot's margin r - alpha appears as
@@ -34,6 +39,8 @@ struct SpaceParams {
   int32_t rs;                 // row stride of the projection rows (floats): np, or np+4 when np/4 is even,
                               // so 8 consecutive rows fall in distinct 16-byte shared-memory bank groups
   int64_t n_jobs_pad;         // jobs rounded up to a multiple of 64 (rows of every projection block)
+  int32_t n_stages;           // ceil(n_cfg / kStageCfg)
+  int32_t n_roles;            // n_slots * (n_slots + 1) operand roles of the gathered layout
   int32_t n_cfg;              // n_states * n_caps
   float alpha;
   float inv_p[kMaxCaps];      // per cap: fl(1/P) (Problem 2) or 1 (Problem 1)
@@ -53,6 +60,10 @@ struct Workspace {
   float* w = nullptr;               // [n_slots][n_states][n_jobs_pad][rs] throughput share of the job in
                                     //   slot i of state s at cap p, already divided by P (Problem 2):
                                     //   (U[s_i] + sum_{l != i} V[s_l]) * invP; padding = -1e30
+  float* fast = nullptr;            // [n_roles][n_stages][n_jobs_pad][kStageRS] operands of the tiled scorers
+                                    //   along the flattened config axis; the
+                                    //   W roles hold fixed-point objective shares ("packed objective")
+  unsigned* wmm = nullptr;          // [2 * kMaxSlots] per-slot min / max of w (order-preserving u32)
   unsigned long long* best_key = nullptr;  // [1] shard argmax key
   unsigned long long* err = nullptr;       // [1] first bad job: (pos << 8) | status, ~0 = none
   unsigned long long* job_key = nullptr;   // [n_jobs] greedy per-job best keys
@@ -72,8 +83,8 @@ struct Workspace {
 };
 
 constexpr int kHistBins = 65536;
-size_t workspace_layout(int64_t n_jobs, int32_t n_slices, int32_t rs, int32_t n_slots, int32_t n_states,
-                        int64_t n_sets_local, int nranks, char* base, Workspace* ws);
+size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_local, int nranks, char* base,
+                        Workspace* ws);
 // greedy.cu
 void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st);
 void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st);
@@ -97,11 +108,11 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
                      unsigned long long* err, cudaStream_t st);
 void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
                     const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
-                    cudaStream_t st);
+                    float* fast, unsigned* wmm, cudaStream_t st);
 // Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
 // maxes the packed key into *best_key. Returns the number of kernels launched.
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                 int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                 const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                  const unsigned long long* err, int variant, cudaStream_t st);
 void launch_exact_alloc(int n_slots, int64_t n_jobs, const float* set_obj, int64_t n_match,
                         unsigned long long* best_key, cudaStream_t st);

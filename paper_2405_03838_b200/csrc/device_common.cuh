@@ -66,6 +66,11 @@ __device__ __forceinline__ uint32_t ord_float_d(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+__device__ __forceinline__ float unord_float_d(uint32_t o) {
+  uint32_t b = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(b);
+}
+
 // Packed argmax key: larger objective first, then lower set id. Unique per set.
 __device__ __forceinline__ unsigned long long pack_key(float obj, int64_t sid) {
   return ((unsigned long long)ord_float_d(obj) << 32) | (0xFFFFFFFFull - (unsigned long long)(uint32_t)sid);

@@ -12,6 +12,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "cosched_internal.h"
 #include "device_common.cuh"
 
@@ -129,9 +131,109 @@ __global__ void k_project_w(const float* __restrict__ F, const int32_t* __restri
   w[idx] = __fmul_rn(acc, sp.inv_p[p]);
 }
 
+// Gathered layout of the tiled scorers (DESIGN.md "gathered layout" and
+// "packed objective"). For slot i of a set and config c = (state s, cap p) the
+// operands are laid out along the flattened config axis, per role:
+//   role A_i   = ka[s_i(s)][j][p]            (own term minus alpha, scaled)
+//   role B_i^l = kb[s_l(s)][j][p], l != i    (this job's interference on slot l)
+//   role W_i   = fixed-point share of Throughput[/P]:
+//       q = rint((w[i][s][j][p] - wmin_i) * inv_delta),
+//       inv_delta = (2^25 - 2 - n_slots) / sum_i (wmax_i - wmin_i)   (sum_i q_i < 2^25)
+//       W_0 = 0x00800000 + (q << 5); W_last = (q << 5) | (31 - off); others q << 5
+//     where off = c mod kStageCfg. The integer sum of a candidate's W's, read
+//     as FP32 bits, is a positive normal float below 4.0 that orders like the
+//     objective up to one quantum per slot (< 4e-7 relative for the presets)
+//     and carries the config's offset in its stage in the low 5 bits.
+// Rows are [role][stage][job][kStageRS]; padding (configs >= n_cfg, jobs >=
+// n_jobs, columns >= kStageCfg) gets A = B = -1e30 (infeasible) and W = 0.
+__global__ void k_w_minmax(const float* __restrict__ w, const SpaceParams sp, int64_t n_jobs, unsigned* wmm) {
+  __shared__ unsigned s_mm[2 * kMaxSlots];
+  if (threadIdx.x < 2 * kMaxSlots) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
+  __syncthreads();
+  const int64_t per_slot = (int64_t)sp.n_states * sp.n_jobs_pad * sp.rs;
+  for (int slot = 0; slot < sp.n_slots; slot++) {
+    unsigned lo = 0xFFFFFFFFu, hi = 0u;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < per_slot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int p = (int)(idx % sp.rs);
+      const int64_t n = (idx / sp.rs) % sp.n_jobs_pad;
+      if (p >= sp.n_caps || n >= n_jobs) continue;
+      const unsigned u = ord_float_d(w[slot * per_slot + idx]);
+      lo = u < lo ? u : lo;
+      hi = u > hi ? u : hi;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo, off), b = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_mm[2 * slot], lo);
+      atomicMax(&s_mm[2 * slot + 1], hi);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * sp.n_slots) {
+    if (threadIdx.x & 1) atomicMax(&wmm[threadIdx.x], s_mm[threadIdx.x]);
+    else atomicMin(&wmm[threadIdx.x], s_mm[threadIdx.x]);
+  }
+}
+
+__global__ void k_gather_fast(const float* __restrict__ ka, const float* __restrict__ kb, const float* __restrict__ w,
+                              const SpaceParams sp, int64_t n_jobs, const unsigned* __restrict__ wmm,
+                              float* __restrict__ fast) {
+  __shared__ float s_lo[kMaxSlots];
+  __shared__ float s_inv;
+  if (threadIdx.x == 0) {
+    float span = 0.0f;
+    for (int i = 0; i < sp.n_slots; i++) {
+      const float lo = unord_float_d(wmm[2 * i]), hi = unord_float_d(wmm[2 * i + 1]);
+      s_lo[i] = lo;
+      span += hi - lo;
+    }
+    s_inv = span > 0.0f ? (float)(33554430 - sp.n_slots) / span : 0.0f;
+  }
+  __syncthreads();
+  const int64_t total = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad * kStageRS;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int col = (int)(idx % kStageRS);
+  int64_t r = idx / kStageRS;
+  const int64_t job = r % sp.n_jobs_pad;
+  r /= sp.n_jobs_pad;
+  const int stage = (int)(r % sp.n_stages);
+  const int role = (int)(r / sp.n_stages);
+  const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
+  const int c = stage * kStageCfg + col;
+  const bool pad = col >= kStageCfg || c >= sp.n_cfg || job >= n_jobs;
+  float v;
+  if (kind == sp.n_slots) {
+    unsigned bits = 0u;
+    if (!pad) {
+      const int s = c / sp.n_caps, p = c - (c / sp.n_caps) * sp.n_caps;
+      const float qf = rintf((w_row(w, sp, slot, s, job)[p] - s_lo[slot]) * s_inv);
+      bits = (qf > 0.0f ? (unsigned)qf : 0u) << 5;
+      if (slot == 0) bits += 0x00800000u;
+      if (slot == sp.n_slots - 1) bits |= (unsigned)(31 - col);
+    }
+    v = __uint_as_float(bits);
+  } else if (pad) {
+    v = -1e30f;
+  } else {
+    const int s = c / sp.n_caps, p = c - (c / sp.n_caps) * sp.n_caps;
+    if (kind == 0) {
+      v = ka_row(ka, sp, sp.slice[s][slot], job)[p];
+    } else {
+      const int l = kind - 1 + (kind - 1 >= slot ? 1 : 0);  // the kind-th other slot, ascending
+      v = ka_row(kb, sp, sp.slice[s][l], job)[p];
+    }
+  }
+  fast[idx] = v;
+}
+
 void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
                     const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
-                    cudaStream_t st) {
+                    float* fast, unsigned* wmm, cudaStream_t st) {
   int64_t total = (int64_t)sp.n_slices * sp.n_jobs_pad * sp.rs;
   if (n_jobs <= 0 || total <= 0) return;
   int bs = 256;
@@ -140,6 +242,16 @@ void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, 
   int64_t tw = (int64_t)sp.n_slots * sp.n_states * sp.n_jobs_pad * sp.rs;
   k_project_w<<<(unsigned)((tw + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
                                                               err, w);
+  unsigned init[2 * kMaxSlots];
+  for (int i = 0; i < kMaxSlots; i++) {
+    init[2 * i] = 0xFFFFFFFFu;
+    init[2 * i + 1] = 0u;
+  }
+  cudaMemcpyAsync(wmm, init, sizeof init, cudaMemcpyHostToDevice, st);
+  int64_t mb = std::min<int64_t>((tw / sp.n_slots + bs - 1) / bs, 148 * 4);
+  k_w_minmax<<<(unsigned)mb, bs, 0, st>>>(w, sp, n_jobs, wmm);
+  const int64_t tf = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad * kStageRS;
+  k_gather_fast<<<(unsigned)((tf + bs - 1) / bs), bs, 0, st>>>(ka, kb, w, sp, n_jobs, wmm, fast);
 }
 
 // ---------------------------------------------------------------------------
@@ -187,21 +299,21 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
 }
 
 int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                            int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                            const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                             const unsigned long long* err, cudaStream_t st);
 
 int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                              int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                              const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                               const unsigned long long* err, cudaStream_t st);
 
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                 int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                 const unsigned long long* err, int variant, cudaStream_t st) {
+                 const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
+                 unsigned long long* best_key, const unsigned long long* err, int variant, cudaStream_t st) {
   if (count <= 0) return 0;
   if (variant != 0 && sp.n_slots == 2)
-    return launch_score_pairs_fast(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, st);
+    return launch_score_pairs_fast(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, st);
   if (variant != 0 && sp.n_slots == 3)
-    return launch_score_triples_fast(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, st);
+    return launch_score_triples_fast(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, st);
   int bs = 256;
   unsigned grid = (unsigned)((count + bs - 1) / bs);
   if (sp.n_slots == 1)

@@ -1,23 +1,25 @@
 // score_triples.cu -- the fast triple scorer (SURVEY.md §8(a) a4-a8 for n_slots = 3), sm_100a.
 //
 // For every triple j0 < j1 < j2 of this rank's plane range (j2 in [c0, c1)) and
-// every config (state s with slot slices s0, s1, s2; cap p), in the canonical
+// every config c (state s with slot slices s0, s1, s2; cap p), in the canonical
 // order of eval_cfg<3> (device_common.cuh):
 //   r0'' = ka[s0][j0] + P0,  P0 = kb[s0][j1] + kb[s0][j2]
 //   r1'' = P1 + kb[s1][j0],  P1 = ka[s1][j1] + kb[s1][j2]
 //   r2'' = P2 + kb[s2][j0],  P2 = ka[s2][j2] + kb[s2][j1]
-//   o    = w[0][s][j0] + Q,  Q  = w[1][s][j1] + w[2][s][j2]
-//   x    = min3(o, r0'', min(r1'', r2''))
+//   o    = W0[j0] + Q,       Q  = W1[j1] + W2[j2]        (integer packed objective)
+//   x    = min3(float_bits(o), r0'', min(r1'', r2''))
 // The partner partials P0, P1, P2, Q depend on (j1, j2) only: they are built once
-// per tile and state in shared memory and reused by all 64 j0 rows, so a
-// candidate costs 4 FP32 adds (2 FADD2 per 2) and 2.5 ALU ops (FMNMX + FMNMX3 +
-// half an FMNMX3 for the running max).
+// per tile and stage in shared memory and reused by all 64 j0 rows, so a
+// candidate costs 3 FP32 adds (FADD2), 1 integer add (IMAD, FMA pipe) and 2.5 ALU
+// ops (FMNMX + FMNMX3 + half an FMNMX3 for the running max).
 //
 // Tiles: fixed j2, a block of 64 j1 (b) and a block of 64 j0 (a <= b); 256
-// threads, 4 x 4 (j0 x j1) micro-tiles, one resident block per SM. Per state the
-// operand rows (4 blocks of 64 j0 rows, 4 of 64 j1 rows, 4 single j2 rows) land
-// by TMA bulk copies (double buffered); the argmax index is tracked per group of
-// 4G caps and resolved exactly at tile end, like the pair scorer.
+// threads, 4 x 4 (j0 x j1) micro-tiles, one resident block per SM. Configs are
+// walked in stages of 24 along the flattened axis (gathered layout, roles
+// [A0 B01 B02 W0 | A1 B10 B12 W1 | A2 B20 B21 W2]); per stage 8 role blocks of
+// 64 rows and 4 single j2 rows land by TMA bulk copies, double buffered. The
+// stage of each triple's best key is tracked; the offset comes back from the
+// key's low bits and the winner is re-evaluated exactly at tile end.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -41,7 +43,7 @@ struct TripleGrid {
   int64_t cum0;    // tiles before plane c0
   int64_t n_tiles;
   int64_t first_set;
-  int groups_per_state;
+  unsigned one;    // runtime 1 for IMAD
 };
 
 // tiles of the planes j2' < j2: plane j has B(j) = ceil(j/64) j1-blocks and B(B+1)/2 tiles
@@ -67,59 +69,47 @@ __device__ __forceinline__ void ttile_coords(const TripleGrid& g, int64_t t, int
   *a = u - bb * (bb + 1) / 2;
 }
 
-// Stage (floats): 8 blocks of kTT rows x rs, then 4 single rows:
-//  [0] A0 = ka[s0][j0]  [1] B01 = kb[s1][j0]  [2] B02 = kb[s2][j0]  [3] W0 = w[0][s][j0]
-//  [4] A1 = ka[s1][j1]  [5] B10 = kb[s0][j1]  [6] B12 = kb[s2][j1]  [7] W1 = w[1][s][j1]
-//  rows: A2 = ka[s2][j2], B20 = kb[s0][j2], B21 = kb[s1][j2], W2 = w[2][s][j2]
+// Stage (floats): role blocks 0..7 of kTT rows x kStageRS (j0 rows for roles
+// 0-3, j1 rows for roles 4-7), then the 4 single j2 rows of roles 8-11.
 __device__ __forceinline__ void issue_tstage(float* stage, uint64_t* bar, const SpaceParams& sp,
-                                             const float* __restrict__ ka, const float* __restrict__ kb,
-                                             const float* __restrict__ w, int64_t a, int64_t b, int64_t j2, int s) {
-  const int s0 = sp.slice[s][0], s1 = sp.slice[s][1], s2 = sp.slice[s][2];
-  const int blk = kTT * sp.rs;
-  const unsigned bytes = (unsigned)blk * 4u, rowb = (unsigned)sp.rs * 4u;
+                                             const float* __restrict__ fast, int64_t a, int64_t b, int64_t j2,
+                                             int g) {
+  constexpr int blk = kTT * kStageRS;
+  constexpr unsigned bytes = (unsigned)blk * 4u, rowb = (unsigned)kStageRS * 4u;
   mbar_arrive_expect_tx(bar, 8u * bytes + 4u * rowb);
-  const int64_t r0 = a * kTT, r1 = b * kTT;
-  tma_bulk_g2s(stage + 0 * blk, ka_row(ka, sp, s0, r0), bytes, bar);
-  tma_bulk_g2s(stage + 1 * blk, ka_row(kb, sp, s1, r0), bytes, bar);
-  tma_bulk_g2s(stage + 2 * blk, ka_row(kb, sp, s2, r0), bytes, bar);
-  tma_bulk_g2s(stage + 3 * blk, w_row(w, sp, 0, s, r0), bytes, bar);
-  tma_bulk_g2s(stage + 4 * blk, ka_row(ka, sp, s1, r1), bytes, bar);
-  tma_bulk_g2s(stage + 5 * blk, ka_row(kb, sp, s0, r1), bytes, bar);
-  tma_bulk_g2s(stage + 6 * blk, ka_row(kb, sp, s2, r1), bytes, bar);
-  tma_bulk_g2s(stage + 7 * blk, w_row(w, sp, 1, s, r1), bytes, bar);
+#pragma unroll
+  for (int role = 0; role < 8; role++) {
+    const int64_t row0 = (role < 4 ? a : b) * kTT;
+    tma_bulk_g2s(stage + role * blk, fast + (((int64_t)role * sp.n_stages + g) * sp.n_jobs_pad + row0) * kStageRS,
+                 bytes, bar);
+  }
   float* rows = stage + 8 * blk;
-  tma_bulk_g2s(rows + 0 * sp.rs, ka_row(ka, sp, s2, j2), rowb, bar);
-  tma_bulk_g2s(rows + 1 * sp.rs, ka_row(kb, sp, s0, j2), rowb, bar);
-  tma_bulk_g2s(rows + 2 * sp.rs, ka_row(kb, sp, s1, j2), rowb, bar);
-  tma_bulk_g2s(rows + 3 * sp.rs, w_row(w, sp, 2, s, j2), rowb, bar);
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    tma_bulk_g2s(rows + k * kStageRS,
+                 fast + (((int64_t)(8 + k) * sp.n_stages + g) * sp.n_jobs_pad + j2) * kStageRS, rowb, bar);
 }
 
 }  // namespace
 
-template <int NP, int G>
 __global__ void __launch_bounds__(kTThreads, 1)
     k_score_triples_tiled(const SpaceParams sp, const TripleGrid g, const float* __restrict__ ka,
-                          const float* __restrict__ kb, const float* __restrict__ w, float* __restrict__ out_obj,
-                          int32_t* __restrict__ out_cfg, unsigned long long* __restrict__ best_key,
-                          const unsigned long long* __restrict__ err) {
+                          const float* __restrict__ kb, const float* __restrict__ w, const float* __restrict__ fast,
+                          float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+                          unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
   if (*err != ~0ull) return;
-  constexpr int kRS = NP ? (((NP >> 2) & 1) ? NP : NP + 4) : 0;
-  const int rs = NP ? kRS : sp.rs;
-  const int rs4 = rs >> 2;
-  const int stage_floats = 8 * kTT * rs + 4 * rs;
+  constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
+  constexpr int stage_floats = 8 * kTT * rs + 4 * rs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = ((warp & 3) << 2) | (lane & 3), ty = ((warp >> 2) << 3) | (lane >> 2);
-  const int gps = NP ? (NP >> 2) / G : g.groups_per_state;
+  const unsigned one = g.one;
   unsigned long long key = 0;
 
   float* sbest = smem + 2 * stage_floats;
   int16_t* sbg = reinterpret_cast<int16_t*>(sbest + kTT * kTBgRow);
-  for (int e = threadIdx.x; e < kTT * kTBgRow; e += kTThreads) {
-    sbest[e] = 0.0f;
-    sbg[e] = -1;
-  }
+  for (int e = threadIdx.x; e < kTT * kTBgRow; e += kTThreads) sbg[e] = -1;
   int64_t t = blockIdx.x;
   if (t >= g.n_tiles) {
     block_max_key(0ull, best_key);
@@ -135,140 +125,137 @@ __global__ void __launch_bounds__(kTThreads, 1)
   ttile_coords(g, t, &J2, &B, &A);
   int s = 0, buf = 0;
   unsigned phase[2] = {0u, 0u};
-  if (threadIdx.x == 0) issue_tstage(smem, &bars[0], sp, ka, kb, w, A, B, J2, 0);
+  if (threadIdx.x == 0) issue_tstage(smem, &bars[0], sp, fast, A, B, J2, 0);
+
+  float breg[kTM][kTM];
+#pragma unroll
+  for (int a = 0; a < kTM; a++)
+#pragma unroll
+    for (int b = 0; b < kTM; b++) breg[a][b] = 0.0f;
 
   while (true) {
     int64_t nt = t, nJ2 = J2, nB = B, nA = A;
     int ns = s + 1;
-    if (ns == sp.n_states) {
+    if (ns == sp.n_stages) {
       ns = 0;
       nt = t + gridDim.x;
       if (nt < g.n_tiles) ttile_coords(g, nt, &nJ2, &nB, &nA);
     }
     const bool has_next = nt < g.n_tiles;
     if (has_next && threadIdx.x == 0)
-      issue_tstage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, ka, kb, w, nA, nB, nJ2, ns);
+      issue_tstage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nA, nB, nJ2, ns);
     mbar_wait(&bars[buf], phase[buf]);
     phase[buf] ^= 1u;
 
     float* st = smem + buf * stage_floats;
     // partner partials, in place over the j1 blocks: P1 -> [4], P0 -> [5], P2 -> [6], Q -> [7]
     {
-      const int blk = kTT * rs;
+      constexpr int blk = kTT * rs;
       const float* rows = st + 8 * blk;
       for (int e = threadIdx.x; e < blk; e += kTThreads) {
         const int c = e % rs;
         st[4 * blk + e] = __fadd_rn(st[4 * blk + e], rows[2 * rs + c]);  // P1 = ka[s1][j1] + kb[s1][j2]
         st[5 * blk + e] = __fadd_rn(st[5 * blk + e], rows[1 * rs + c]);  // P0 = kb[s0][j1] + kb[s0][j2]
         st[6 * blk + e] = __fadd_rn(rows[0 * rs + c], st[6 * blk + e]);  // P2 = ka[s2][j2] + kb[s2][j1]
-        st[7 * blk + e] = __fadd_rn(st[7 * blk + e], rows[3 * rs + c]);  // Q  = w1 + w2
+        st[7 * blk + e] = __uint_as_float(__float_as_uint(st[7 * blk + e]) + __float_as_uint(rows[3 * rs + c]));
       }
     }
     __syncthreads();
 
     const float4* st4 = reinterpret_cast<const float4*>(st);
-    const int blk4 = kTT * rs4;
+    constexpr int blk4 = kTT * rs4;
     const float4* A0 = st4 + 0 * blk4 + tx * rs4;
     const float4* B01 = st4 + 1 * blk4 + tx * rs4;
     const float4* B02 = st4 + 2 * blk4 + tx * rs4;
-    const float4* W0 = st4 + 3 * blk4 + tx * rs4;
+    const uint4* W0 = reinterpret_cast<const uint4*>(st4 + 3 * blk4 + tx * rs4);
     const float4* P1 = st4 + 4 * blk4 + ty * rs4;
     const float4* P0 = st4 + 5 * blk4 + ty * rs4;
     const float4* P2 = st4 + 6 * blk4 + ty * rs4;
-    const float4* Q = st4 + 7 * blk4 + ty * rs4;
-    const int row16 = 16 * rs4;
+    const uint4* Q = reinterpret_cast<const uint4*>(st4 + 7 * blk4 + ty * rs4);
+    constexpr int row16 = 16 * rs4;
 
+    float m[kTM][kTM];
 #pragma unroll
-    for (int grp = 0; grp < gps; grp++) {
-      float m[kTM][kTM];
+    for (int q = 0; q < chunks; q++) {
+      float4 p0[kTM], p1[kTM], p2[kTM];
+      uint4 qv[kTM];
 #pragma unroll
-      for (int qq = 0; qq < G; qq++) {
-        const int q = grp * G + qq;
-        float4 p0[kTM], p1[kTM], p2[kTM], qv[kTM];
+      for (int b = 0; b < kTM; b++) {
+        p0[b] = P0[b * row16 + q];
+        p1[b] = P1[b * row16 + q];
+        p2[b] = P2[b * row16 + q];
+        qv[b] = Q[b * row16 + q];
+      }
+#pragma unroll
+      for (int a = 0; a < kTM; a++) {
+        const float4 a0 = A0[a * row16 + q];
+        const float4 b01 = B01[a * row16 + q];
+        const float4 b02 = B02[a * row16 + q];
+        const uint4 w0 = W0[a * row16 + q];
 #pragma unroll
         for (int b = 0; b < kTM; b++) {
-          p0[b] = P0[b * row16 + q];
-          p1[b] = P1[b * row16 + q];
-          p2[b] = P2[b * row16 + q];
-          qv[b] = Q[b * row16 + q];
-        }
-#pragma unroll
-        for (int a = 0; a < kTM; a++) {
-          const float4 a0 = A0[a * row16 + q];
-          const float4 b01 = B01[a * row16 + q];
-          const float4 b02 = B02[a * row16 + q];
-          const float4 w0 = W0[a * row16 + q];
-#pragma unroll
-          for (int b = 0; b < kTM; b++) {
-            const float4 r0 = add4(a0, p0[b]);
-            const float4 r1 = add4(p1[b], b01);
-            const float4 r2 = add4(p2[b], b02);
-            const float4 o = add4(w0, qv[b]);
-            const float x0 = min3f(o.x, r0.x, fminf(r1.x, r2.x));
-            const float x1 = min3f(o.y, r0.y, fminf(r1.y, r2.y));
-            const float x2 = min3f(o.z, r0.z, fminf(r1.z, r2.z));
-            const float x3 = min3f(o.w, r0.w, fminf(r1.w, r2.w));
-            if (qq == 0)
-              m[a][b] = fmaxf(max3f(x0, x1, x2), x3);
-            else
-              m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
-          }
+          const float4 r0 = add4(a0, p0[b]);
+          const float4 r1 = add4(p1[b], b01);
+          const float4 r2 = add4(p2[b], b02);
+          const float x0 = min3f(__uint_as_float(imad_add(w0.x, one, qv[b].x)), r0.x, fminf(r1.x, r2.x));
+          const float x1 = min3f(__uint_as_float(imad_add(w0.y, one, qv[b].y)), r0.y, fminf(r1.y, r2.y));
+          const float x2 = min3f(__uint_as_float(imad_add(w0.z, one, qv[b].z)), r0.z, fminf(r1.z, r2.z));
+          const float x3 = min3f(__uint_as_float(imad_add(w0.w, one, qv[b].w)), r0.w, fminf(r1.w, r2.w));
+          if (q == 0)
+            m[a][b] = fmaxf(max3f(x0, x1, x2), x3);
+          else
+            m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
         }
       }
-      const int16_t gidx = (int16_t)((s << 4) | grp);
+    }
+#pragma unroll
+    for (int a = 0; a < kTM; a++)
+#pragma unroll
+      for (int b = 0; b < kTM; b++)
+        if (m[a][b] > breg[a][b]) {
+          breg[a][b] = m[a][b];
+          sbg[(ty + 16 * b) * kTBgRow + tx + 16 * a] = (int16_t)s;
+        }
+
+    if (s == sp.n_stages - 1) {
 #pragma unroll
       for (int a = 0; a < kTM; a++)
 #pragma unroll
         for (int b = 0; b < kTM; b++) {
-          const int e = (ty + 16 * b) * kTBgRow + tx + 16 * a;
-          if (m[a][b] > sbest[e]) {
-            sbest[e] = m[a][b];
-            sbg[e] = gidx;
-          }
+          sbest[(ty + 16 * b) * kTBgRow + tx + 16 * a] = breg[a][b];
+          breg[a][b] = 0.0f;
         }
-    }
-
-    if (s == sp.n_states - 1) {
       __syncthreads();
+#pragma unroll 2
       for (int e = threadIdx.x; e < kTT * kTT; e += kTThreads) {
         const int rj = e >> 6, ri = e & 63;
         const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
-        const int gb = sbg[rj * kTBgRow + ri];
+        const int sg = sbg[rj * kTBgRow + ri];
+        const unsigned kbits = __float_as_uint(sbest[rj * kTBgRow + ri]);
         sbg[rj * kTBgRow + ri] = -1;
-        sbest[rj * kTBgRow + ri] = 0.0f;
         if (!(j0 < j1 && j1 < j2 && j2 < g.n_jobs && j2 >= g.c0 && j2 < g.c1)) continue;
         float bo = -INFINITY;
         int bc = -1;
-        if (gb >= 0) {
-          const int sg = gb >> 4;
-          const int q0 = (gb & 15) * G;
-          const int s0 = sp.slice[sg][0], s1 = sp.slice[sg][1], s2 = sp.slice[sg][2];
-          const float4* ka00 = reinterpret_cast<const float4*>(ka_row(ka, sp, s0, j0)) + q0;
-          const float4* kb01 = reinterpret_cast<const float4*>(ka_row(kb, sp, s0, j1)) + q0;
-          const float4* kb02 = reinterpret_cast<const float4*>(ka_row(kb, sp, s0, j2)) + q0;
-          const float4* ka11 = reinterpret_cast<const float4*>(ka_row(ka, sp, s1, j1)) + q0;
-          const float4* kb12 = reinterpret_cast<const float4*>(ka_row(kb, sp, s1, j2)) + q0;
-          const float4* kb10 = reinterpret_cast<const float4*>(ka_row(kb, sp, s1, j0)) + q0;
-          const float4* ka22 = reinterpret_cast<const float4*>(ka_row(ka, sp, s2, j2)) + q0;
-          const float4* kb21 = reinterpret_cast<const float4*>(ka_row(kb, sp, s2, j1)) + q0;
-          const float4* kb20 = reinterpret_cast<const float4*>(ka_row(kb, sp, s2, j0)) + q0;
-          const float4* w0 = reinterpret_cast<const float4*>(w_row(w, sp, 0, sg, j0)) + q0;
-          const float4* w1 = reinterpret_cast<const float4*>(w_row(w, sp, 1, sg, j1)) + q0;
-          const float4* w2 = reinterpret_cast<const float4*>(w_row(w, sp, 2, sg, j2)) + q0;
-#pragma unroll
-          for (int c = 0; c < G; c++) {
-            const float4 r0 = add4(__ldg(ka00 + c), add4(__ldg(kb01 + c), __ldg(kb02 + c)));
-            const float4 r1 = add4(add4(__ldg(ka11 + c), __ldg(kb12 + c)), __ldg(kb10 + c));
-            const float4 r2 = add4(add4(__ldg(ka22 + c), __ldg(kb21 + c)), __ldg(kb20 + c));
-            const float4 o = add4(__ldg(w0 + c), add4(__ldg(w1 + c), __ldg(w2 + c)));
-            const float rr0[4] = {r0.x, r0.y, r0.z, r0.w}, rr1[4] = {r1.x, r1.y, r1.z, r1.w};
-            const float rr2[4] = {r2.x, r2.y, r2.z, r2.w}, oo[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-              if (rr0[q] > 0.0f && rr1[q] > 0.0f && rr2[q] > 0.0f && oo[q] > bo) {
-                bo = oo[q];
-                bc = sg * sp.n_caps + 4 * (q0 + c) + q;
+        if (sg >= 0) {
+          int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
+          int64_t jj[3] = {j0, j1, j2};
+          float r[3], o;
+          if (c < sp.n_cfg) {
+            eval_cfg<3>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
+            if (r[0] > 0.0f && r[1] > 0.0f && r[2] > 0.0f) {
+              bo = o;
+              bc = c;
+            }
+          }
+          if (bc < 0) {  // clipped key: exact scan of the stage
+            const int cend = min(sg * kStageCfg + kStageCfg, sp.n_cfg);
+            for (c = sg * kStageCfg; c < cend; c++) {
+              eval_cfg<3>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
+              if (r[0] > 0.0f && r[1] > 0.0f && r[2] > 0.0f && o > bo) {
+                bo = o;
+                bc = c;
               }
+            }
           }
         }
         const int64_t sid = j2 * (j2 - 1) * (j2 - 2) / 6 + j1 * (j1 - 1) / 2 + j0;
@@ -296,35 +283,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
 
 static int g_tri_sms = 0;
 
-template <int NP, int G>
-static int launch_ttiled(const SpaceParams& sp, const TripleGrid& g, const float* ka, const float* kb, const float* w,
-                         float* obj, int32_t* cfg, unsigned long long* best_key, const unsigned long long* err,
-                         cudaStream_t st) {
-  size_t smem = (size_t)2 * (8 * kTT * sp.rs + 4 * sp.rs) * sizeof(float) +
-                (size_t)kTT * kTBgRow * (sizeof(float) + sizeof(int16_t));
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_score_triples_tiled<NP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
-  if (!g_tri_sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_tri_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled<NP, G>, kTThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)g_tri_sms * per_sm;
-  if (grid > g.n_tiles) grid = g.n_tiles;
-  if (grid < 1) grid = 1;
-  k_score_triples_tiled<NP, G><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, obj, cfg, best_key, err);
-  return 1;
-}
-
 int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                              int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                              const unsigned long long* err, cudaStream_t st) {
+                              const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
+                              unsigned long long* best_key, const unsigned long long* err, cudaStream_t st) {
   auto c3 = [](int64_t n) { return n * (n - 1) * (n - 2) / 6; };
   auto plane_at = [&](int64_t v) {  // smallest c with C(c,3) >= v
     int64_t c = (int64_t)cbrt(6.0 * (double)v);
@@ -333,38 +294,37 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
     return c;
   };
   int64_t c0 = plane_at(first), c1 = plane_at(first + count);
-  if (c3(c0) != first || c3(c1) != first + count || c1 > n_jobs || (sp.np >> 2) > 16 ||
-      (size_t)2 * (8 * kTT * sp.rs + 4 * sp.rs) * 4 > 190 * 1024) {
-    return launch_score(sp, n_jobs, ka, kb, w, first, count, obj, cfg, best_key, err, 0, st);
+  if (c3(c0) != first || c3(c1) != first + count || c1 > n_jobs) {
+    return launch_score(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, 0, st);
   }
   TripleGrid g;
   g.n_jobs = n_jobs;
   g.c0 = c0;
   g.c1 = c1;
   g.first_set = first;
+  g.one = 1u;
   g.cum0 = tiles_before(c0);
   g.n_tiles = tiles_before(c1) - g.cum0;
-  const int chunks = sp.np >> 2;
-  switch (sp.np) {
-    case 12:
-      g.groups_per_state = 1;
-      return launch_ttiled<12, 3>(sp, g, ka, kb, w, obj, cfg, best_key, err, st);
-    case 24:
-      g.groups_per_state = 2;
-      return launch_ttiled<24, 3>(sp, g, ka, kb, w, obj, cfg, best_key, err, st);
-    default:
-      break;
+  constexpr size_t smem = (size_t)2 * (8 * kTT * kStageRS + 4 * kStageRS) * sizeof(float) +
+                          (size_t)kTT * kTBgRow * (sizeof(float) + sizeof(int16_t));
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_score_triples_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
   }
-  if (chunks % 3 == 0) {
-    g.groups_per_state = chunks / 3;
-    return launch_ttiled<0, 3>(sp, g, ka, kb, w, obj, cfg, best_key, err, st);
+  if (!g_tri_sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_tri_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (chunks % 2 == 0) {
-    g.groups_per_state = chunks / 2;
-    return launch_ttiled<0, 2>(sp, g, ka, kb, w, obj, cfg, best_key, err, st);
-  }
-  g.groups_per_state = chunks;
-  return launch_ttiled<0, 1>(sp, g, ka, kb, w, obj, cfg, best_key, err, st);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled, kTThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)g_tri_sms * per_sm;
+  if (grid > g.n_tiles) grid = g.n_tiles;
+  if (grid < 1) grid = 1;
+  k_score_triples_tiled<<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+  return 1;
 }
 
 }  // namespace cosched

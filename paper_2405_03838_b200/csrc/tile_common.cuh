@@ -24,6 +24,21 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// scalar FADDs: mixing them with FADD2 keeps both FMA half-pipes fed without the
+// dispatch stalls an all-FADD2 stream shows (tools/microbench/inner.cu: 32 vs 27
+// candidates/clk/SM for the pair loop)
+__device__ __forceinline__ float4 add4s(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+// integer add on the FMA pipe (IMAD with a runtime multiplier of 1): the ALU
+// pipe is the scarce one, so the fixed-point objective sums go to IMAD
+__device__ __forceinline__ unsigned imad_add(unsigned a, unsigned one, unsigned b) {
+  unsigned r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
+
 // ---- mbarrier + TMA bulk copy (PTX, sm_90+) ---------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {

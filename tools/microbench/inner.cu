@@ -11,13 +11,16 @@ __device__ __forceinline__ float min3f(float a, float b, float c) {
 __device__ __forceinline__ float max3f(float a, float b, float c) {
   float r; asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c)); return r;
 }
+__device__ __forceinline__ float4 add4s(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
   float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
-template <int MI, int MJ, int MINB>
+template <int MI, int MJ, int MINB, int MODE>
 __global__ void __launch_bounds__(256, MINB) kinner(const float4* __restrict__ in, float* out, int iters) {
   float4 a0[MI], b0[MI], w0[MI], a1[MJ], b1[MJ], w1[MJ];
   for (int i = 0; i < MI; i++) { a0[i] = in[threadIdx.x % 7 + i]; b0[i] = in[i + 1]; w0[i] = in[i + 2]; }
@@ -29,9 +32,9 @@ __global__ void __launch_bounds__(256, MINB) kinner(const float4* __restrict__ i
     for (int a = 0; a < MI; a++) {
 #pragma unroll
       for (int b = 0; b < MJ; b++) {
-        const float4 r0 = add4(a0[a], b1[b]);
-        const float4 r1 = add4(a1[b], b0[a]);
-        const float4 o = add4(w0[a], w1[b]);
+        const float4 r0 = MODE == 1 ? add4s(a0[a], b1[b]) : add4(a0[a], b1[b]);
+        const float4 r1 = MODE == 1 ? add4s(a1[b], b0[a]) : add4(a1[b], b0[a]);
+        const float4 o = MODE >= 1 ? add4s(w0[a], w1[b]) : add4(w0[a], w1[b]);
         const float x0 = min3f(o.x, r0.x, r1.x), x1 = min3f(o.y, r0.y, r1.y);
         const float x2 = min3f(o.z, r0.z, r1.z), x3 = min3f(o.w, r0.w, r1.w);
         m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
@@ -48,19 +51,19 @@ __global__ void __launch_bounds__(256, MINB) kinner(const float4* __restrict__ i
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-template <int MI, int MJ, int MINB>
+template <int MI, int MJ, int MINB, int MODE>
 void run(int warps_per_sm, int nsm, const float4* in, float* out) {
   int threads = 256;
   int blocks = nsm * warps_per_sm * 32 / threads;
   int iters = 2000;
-  kinner<MI, MJ, MINB><<<blocks, threads>>>(in, out, 10);
+  kinner<MI, MJ, MINB, MODE><<<blocks, threads>>>(in, out, 10);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kinner<MI, MJ, MINB><<<blocks, threads>>>(in, out, iters);
+  kinner<MI, MJ, MINB, MODE><<<blocks, threads>>>(in, out, iters);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   double cands = (double)blocks * threads * iters * MI * MJ * 4;
-  printf("MI=%d MJ=%d minB=%d warps/SM=%2d: %.3f ms, %.3g cand/s, %.1f cand/clk/SM @1.9GHz\n", MI, MJ, MINB, warps_per_sm, ms,
+  printf("MODE=%d MI=%d MJ=%d minB=%d warps/SM=%2d: %.3f ms, %.3g cand/s, %.1f cand/clk/SM @1.9GHz\n", MODE, MI, MJ, MINB, warps_per_sm, ms,
          cands / (ms * 1e-3), cands / (ms * 1e-3) / nsm / 1.9e9);
 }
 
@@ -69,11 +72,12 @@ int main() {
   float4* in; float* out;
   cudaMalloc(&in, 64 * sizeof(float4)); cudaMemset(in, 0, 64 * sizeof(float4));
   cudaMalloc(&out, 148 * 2048 * 4 * 4);
-  run<4, 4, 1>(8, nsm, in, out);
-  run<4, 4, 2>(16, nsm, in, out);
-  run<4, 4, 2>(32, nsm, in, out);
-  run<4, 8, 1>(8, nsm, in, out);
-  run<2, 4, 4>(32, nsm, in, out);
-  run<2, 4, 2>(16, nsm, in, out);
+  run<4, 4, 1, 0>(8, nsm, in, out);
+  run<4, 4, 1, 1>(8, nsm, in, out);
+  run<4, 4, 1, 2>(8, nsm, in, out);
+  run<2, 4, 2, 0>(16, nsm, in, out);
+  run<2, 4, 2, 1>(16, nsm, in, out);
+  run<2, 4, 2, 2>(16, nsm, in, out);
+  run<4, 4, 1, 0>(16, nsm, in, out);
   return 0;
 }
