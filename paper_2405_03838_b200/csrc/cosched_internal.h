@@ -16,10 +16,11 @@ constexpr int kMaxStates = 128;
 constexpr int kMaxSlices = 128;
 constexpr int kMaxSlots = 3;
 // The tiled scorers walk the flattened config space c = state * n_caps + cap in
-// stages of kStageCfg consecutive configs; each stage row is padded to kStageRS
-// floats (7 float4: odd, so 8 consecutive rows hit distinct shared-memory bank groups).
-constexpr int kStageCfg = 24;
-constexpr int kStageRS = 28;
+// stages of kStageCfg consecutive configs; each stage row is kStageRS floats
+// (5 float4: odd, so 8 consecutive rows hit distinct shared-memory bank groups).
+// 20 keeps the padding of the last stage small (294 configs -> 300, 882 -> 900).
+constexpr int kStageCfg = 20;
+constexpr int kStageRS = 20;
 
 // Feasibility scale: the projection stores
 // K*(U - alpha) and K*V, so a slot's margin r - alpha appears as

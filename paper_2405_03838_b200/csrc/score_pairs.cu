@@ -13,7 +13,7 @@
 // the winner is re-evaluated exactly in FP32 at tile end.
 //
 // Design (DESIGN.md §5 "Pair scorer"):
-//  - persistent CTAs (one per SM, 8 warps, ~160 registers per thread) walk 64x64
+//  - persistent CTAs (two per SM, 16 warps, 128 registers per thread) walk 64x64
 //    tiles of the pair triangle; each thread owns a 4x4 register micro-tile
 //    (j0 = tx + 16a, j1 = ty + 16b); a warp covers 4 j0 x 8 j1 rows, so every
 //    float4 operand load is one shared-memory wavefront;
@@ -80,7 +80,8 @@ __device__ __forceinline__ void issue_stage(float* stage, uint64_t* bar, const S
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ ka,
                         const float* __restrict__ kb, const float* __restrict__ w, const float* __restrict__ fast,
                         float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
@@ -285,10 +286,12 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   g.n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - g.base;
   constexpr size_t smem = (size_t)2 * 6 * kTile * kStageRS * sizeof(float) +
                           (size_t)kTile * kBgRow * (sizeof(float) + sizeof(int16_t));
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_score_pairs_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+  static int minb = -1;
+  if (minb < 0) {
+    const char* e = getenv("COSCHED_PAIR_MINB");
+    minb = (e && e[0] == '1') ? 1 : 2;
+    cudaFuncSetAttribute(k_score_pairs_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_pairs_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   if (!g_num_sms) {
     int dev;
@@ -296,12 +299,16 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled, kThreads, smem);
+  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1>, kThreads, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2>, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)g_num_sms * per_sm;
   if (grid > g.n_tiles) grid = g.n_tiles;
   if (grid < 1) grid = 1;
-  k_score_pairs_tiled<<<(unsigned)grid, kThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+  if (minb == 1)
+    k_score_pairs_tiled<1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+  else
+    k_score_pairs_tiled<2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
   return 1;
 }
 
