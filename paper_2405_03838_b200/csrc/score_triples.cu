@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "cosched_internal.h"
 #include "device_common.cuh"
@@ -92,7 +93,8 @@ __device__ __forceinline__ void issue_tstage(float* stage, uint64_t* bar, const 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTThreads, 1)
+template <int MINB>
+__global__ void __launch_bounds__(kTThreads, MINB)
     k_score_triples_tiled(const SpaceParams sp, const TripleGrid g, const float* __restrict__ ka,
                           const float* __restrict__ kb, const float* __restrict__ w, const float* __restrict__ fast,
                           float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
@@ -307,10 +309,12 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
   g.n_tiles = tiles_before(c1) - g.cum0;
   constexpr size_t smem = (size_t)2 * (8 * kTT * kStageRS + 4 * kStageRS) * sizeof(float) +
                           (size_t)kTT * kTBgRow * (sizeof(float) + sizeof(int16_t));
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_score_triples_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+  static int minb = -1;
+  if (minb < 0) {
+    const char* e = getenv("COSCHED_TRIPLE_MINB");
+    minb = (e && e[0] == '1') ? 1 : 2;
+    cudaFuncSetAttribute(k_score_triples_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_triples_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   if (!g_tri_sms) {
     int dev;
@@ -318,12 +322,16 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
     cudaDeviceGetAttribute(&g_tri_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled, kTThreads, smem);
+  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled<1>, kTThreads, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled<2>, kTThreads, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)g_tri_sms * per_sm;
   if (grid > g.n_tiles) grid = g.n_tiles;
   if (grid < 1) grid = 1;
-  k_score_triples_tiled<<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+  if (minb == 1)
+    k_score_triples_tiled<1><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+  else
+    k_score_triples_tiled<2><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
   return 1;
 }
 
