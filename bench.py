@@ -45,6 +45,21 @@ ALU_LANES_PER_SM_CLK = 64
 N_SM = 148
 
 
+def _traffic(workload: str, n_slots: int):
+    """DRAM bytes per scorer launch from the committed ncu --set full capture
+    (profiles/<round>/<workload>_scorer_ncu_summary.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"{workload.lower()}_scorer_ncu_summary.json")),
+                       reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            return float(d["traffic_bytes_per_launch"]) / 1e9, os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -290,6 +305,7 @@ def run_ours(args):
         score_avg_ms = score_total / args.steps
         local_cand = count * n_cfg  # per-rank candidates of one scorer launch (rank 0's shard)
         ops = ALU_OPS_PER_CAND[pb.n_slots]
+        traffic_gb, traffic_src = _traffic(args.config, pb.n_slots)
         achieved = local_cand * ops / (score_avg_ms * 1e-3) / 1e12
         clocks = clk.summary()
         line = {
@@ -303,7 +319,9 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MB write)",
                        "scorer": "fast" if (args.variant is None or args.variant == 1) else "generic"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-ops/s",
-                         "frac": achieved / alu_peak, "traffic": None,
+                         "frac": achieved / alu_peak, "traffic": traffic_gb, "traffic_unit": "GB per launch",
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch_gb": count * 8 / 1e9,
                          "kernel": "set scorer", "ops_per_candidate": ops,
                          "kernel_ms": score_avg_ms, "kernel_share_of_step": score_avg_ms / ms_per_step,
                          "peak_source": f"148 SM x 64 ALU lanes x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)"},

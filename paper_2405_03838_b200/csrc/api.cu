@@ -552,7 +552,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, st);
     launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
-    h->launches += 5;
+    h->launches += 4;
   }
   cudaEventRecord(h->ev[1], st);
   h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);

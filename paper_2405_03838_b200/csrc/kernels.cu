@@ -73,62 +73,102 @@ __device__ __forceinline__ float dot_v(const float* __restrict__ D, const float 
   return v;
 }
 
-__global__ void k_project(const float* __restrict__ F, const int32_t* __restrict__ jobs, int64_t n_jobs,
-                          const SpaceParams sp, const float* __restrict__ coef_c,
-                          const float* __restrict__ coef_d, const unsigned long long* __restrict__ err,
-                          float* __restrict__ ka, float* __restrict__ kb) {
-  if (*err != ~0ull) return;  // invalid input: leave the workspace untouched
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t total = (int64_t)sp.n_slices * sp.n_jobs_pad * sp.rs;
-  if (idx >= total) return;
-  int p = (int)(idx % sp.rs);
-  int64_t r = idx / sp.rs;
-  int64_t n = r % sp.n_jobs_pad;
-  int s = (int)(r / sp.n_jobs_pad);
-  if (p >= sp.n_caps || n >= n_jobs) {
-    ka[idx] = -1e30f;
-    kb[idx] = -1e30f;
-    return;
-  }
-  int64_t row = jobs ? (int64_t)jobs[n] : n;
+// Row-per-warp projection: a warp owns one row of a projection array and its
+// lanes are the caps p (coalesced 4-byte stores); every lane recomputes the
+// job's basis (3 divisions), which is cheaper than sharing it. One launch
+// writes the ka/kb rows ([slice][job]), the w rows ([slot][state][job]) and the
+// per-slot min/max of w (warp + block reduction, then one atomic per block).
+__device__ __forceinline__ void wrow_value(const float* __restrict__ F, const int32_t* __restrict__ jobs,
+                                           const SpaceParams& sp, const float* __restrict__ coef_c,
+                                           const float* __restrict__ coef_d, int64_t n, int slot, int s, int p,
+                                           float* out) {
+  const int64_t row = jobs ? (int64_t)jobs[n] : n;
   float h[6], j[3];
   basis_hj(F + row * 8, h, j);
-  float u = dot_u(coef_c + ((int64_t)p * sp.n_slices + s) * 6, h);
-  float v = dot_v(coef_d + ((int64_t)p * sp.n_slices + s) * 3, j);
-  ka[idx] = __fmul_rn(__fsub_rn(u, sp.alpha), kScale);
-  kb[idx] = __fmul_rn(v, kScale);
+  float acc = dot_u(coef_c + ((int64_t)p * sp.n_slices + sp.slice[s][slot]) * 6, h);
+  for (int l = 0; l < sp.n_slots; l++)
+    if (l != slot) acc = __fadd_rn(acc, dot_v(coef_d + ((int64_t)p * sp.n_slices + sp.slice[s][l]) * 3, j));
+  *out = __fmul_rn(acc, sp.inv_p[p]);
 }
 
-// Throughput share of job n when it sits in slot i of state s at cap p. The
-// model's Throughput = sum_i RPerf_i = sum_i (U[j_i][s_i] + sum_{l!=i} V[j_l][s_i])
-// regroups exactly per job as sum_i (U[j_i][s_i] + sum_{l!=i} V[j_i][s_l]), so
-//   w[n][i][s][p] = (U_n[s_i] + sum_{l != i} V_n[s_l]) * invP   (left-to-right sums)
-// and a candidate's objective is the FP32 sum of its jobs' shares in slot order.
-__global__ void k_project_w(const float* __restrict__ F, const int32_t* __restrict__ jobs, int64_t n_jobs,
-                            const SpaceParams sp, const float* __restrict__ coef_c,
-                            const float* __restrict__ coef_d, const unsigned long long* __restrict__ err,
-                            float* __restrict__ w) {
-  if (*err != ~0ull) return;
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t total = (int64_t)sp.n_slots * sp.n_states * sp.n_jobs_pad * sp.rs;
-  if (idx >= total) return;
-  int p = (int)(idx % sp.rs);
-  int64_t r = idx / sp.rs;
-  int64_t n = r % sp.n_jobs_pad;
-  r /= sp.n_jobs_pad;
-  int s = (int)(r % sp.n_states);
-  int i = (int)(r / sp.n_states);
-  if (p >= sp.n_caps || n >= n_jobs) {
-    w[idx] = -1e30f;
-    return;
+__global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F, const int32_t* __restrict__ jobs,
+                                                     int64_t n_jobs, const SpaceParams sp,
+                                                     const float* __restrict__ coef_c,
+                                                     const float* __restrict__ coef_d,
+                                                     const unsigned long long* __restrict__ err,
+                                                     float* __restrict__ ka, float* __restrict__ kb,
+                                                     float* __restrict__ w, unsigned* wmm) {
+  __shared__ unsigned s_mm[2 * kMaxSlots];
+  if (threadIdx.x < 2 * kMaxSlots) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
+  __syncthreads();
+  if (*err != ~0ull) return;  // invalid input: leave the workspace untouched (uniform per launch)
+  const int lane = threadIdx.x & 31;
+  const unsigned npad = (unsigned)sp.n_jobs_pad;
+  const unsigned rows_k = (unsigned)sp.n_slices * npad;
+  const unsigned rows_w = (unsigned)(sp.n_slots * sp.n_states) * npad;
+  const unsigned wpb = blockDim.x >> 5;
+  unsigned lo[kMaxSlots], hi[kMaxSlots];
+#pragma unroll
+  for (int i = 0; i < kMaxSlots; i++) {
+    lo[i] = 0xFFFFFFFFu;
+    hi[i] = 0u;
   }
-  int64_t row = jobs ? (int64_t)jobs[n] : n;
-  float h[6], j[3];
-  basis_hj(F + row * 8, h, j);
-  float acc = dot_u(coef_c + ((int64_t)p * sp.n_slices + sp.slice[s][i]) * 6, h);
-  for (int l = 0; l < sp.n_slots; l++)
-    if (l != i) acc = __fadd_rn(acc, dot_v(coef_d + ((int64_t)p * sp.n_slices + sp.slice[s][l]) * 3, j));
-  w[idx] = __fmul_rn(acc, sp.inv_p[p]);
+  for (unsigned r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows_k + rows_w; r += gridDim.x * wpb) {
+    for (int p = lane; p < sp.rs; p += 32) {
+      if (r < rows_k) {
+        const unsigned s = r / npad, n = r - s * npad;
+        const size_t o = (size_t)r * sp.rs + p;
+        if (p >= sp.n_caps || n >= n_jobs) {
+          ka[o] = -1e30f;
+          kb[o] = -1e30f;
+          continue;
+        }
+        const int64_t row = jobs ? (int64_t)jobs[n] : (int64_t)n;
+        float h[6], j[3];
+        basis_hj(F + row * 8, h, j);
+        const float u = dot_u(coef_c + ((int64_t)p * sp.n_slices + s) * 6, h);
+        const float v = dot_v(coef_d + ((int64_t)p * sp.n_slices + s) * 3, j);
+        ka[o] = __fmul_rn(__fsub_rn(u, sp.alpha), kScale);
+        kb[o] = __fmul_rn(v, kScale);
+      } else {
+        const unsigned rw = r - rows_k;
+        const unsigned n = rw % npad, ss = rw / npad;
+        const int slot = (int)(ss / sp.n_states), s = (int)(ss % sp.n_states);
+        const size_t o = (size_t)rw * sp.rs + p;
+        if (p >= sp.n_caps || n >= n_jobs) {
+          w[o] = -1e30f;
+          continue;
+        }
+        float v;
+        wrow_value(F, jobs, sp, coef_c, coef_d, n, slot, s, p, &v);
+        w[o] = v;
+        const unsigned uo = ord_float_d(v);
+#pragma unroll
+        for (int i = 0; i < kMaxSlots; i++)
+          if (i == slot) {
+            lo[i] = uo < lo[i] ? uo : lo[i];
+            hi[i] = uo > hi[i] ? uo : hi[i];
+          }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxSlots; i++) {
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo[i], off), b = __shfl_xor_sync(0xFFFFFFFFu, hi[i], off);
+      lo[i] = a < lo[i] ? a : lo[i];
+      hi[i] = b > hi[i] ? b : hi[i];
+    }
+    if (lane == 0 && i < sp.n_slots) {
+      atomicMin(&s_mm[2 * i], lo[i]);
+      atomicMax(&s_mm[2 * i + 1], hi[i]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * sp.n_slots) {
+    if (threadIdx.x & 1) atomicMax(&wmm[threadIdx.x], s_mm[threadIdx.x]);
+    else atomicMin(&wmm[threadIdx.x], s_mm[threadIdx.x]);
+  }
 }
 
 // Gathered layout of the tiled scorers (DESIGN.md "gathered layout" and
@@ -145,43 +185,13 @@ __global__ void k_project_w(const float* __restrict__ F, const int32_t* __restri
 //     objective up to one quantum per slot (< 4e-7 relative for the presets)
 //     and carries the config's offset in its stage in the low 5 bits.
 // Rows are [role][stage][job][kStageRS]; padding (configs >= n_cfg, jobs >=
-// n_jobs, columns >= kStageCfg) gets A = B = -1e30 (infeasible) and W = 0.
-__global__ void k_w_minmax(const float* __restrict__ w, const SpaceParams sp, int64_t n_jobs, unsigned* wmm) {
-  __shared__ unsigned s_mm[2 * kMaxSlots];
-  if (threadIdx.x < 2 * kMaxSlots) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
-  __syncthreads();
-  const int64_t per_slot = (int64_t)sp.n_states * sp.n_jobs_pad * sp.rs;
-  for (int slot = 0; slot < sp.n_slots; slot++) {
-    unsigned lo = 0xFFFFFFFFu, hi = 0u;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < per_slot;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-      const int p = (int)(idx % sp.rs);
-      const int64_t n = (idx / sp.rs) % sp.n_jobs_pad;
-      if (p >= sp.n_caps || n >= n_jobs) continue;
-      const unsigned u = ord_float_d(w[slot * per_slot + idx]);
-      lo = u < lo ? u : lo;
-      hi = u > hi ? u : hi;
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      const unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo, off), b = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
-      lo = a < lo ? a : lo;
-      hi = b > hi ? b : hi;
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(&s_mm[2 * slot], lo);
-      atomicMax(&s_mm[2 * slot + 1], hi);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 2 * sp.n_slots) {
-    if (threadIdx.x & 1) atomicMax(&wmm[threadIdx.x], s_mm[threadIdx.x]);
-    else atomicMin(&wmm[threadIdx.x], s_mm[threadIdx.x]);
-  }
-}
-
-__global__ void k_gather_fast(const float* __restrict__ ka, const float* __restrict__ kb, const float* __restrict__ w,
-                              const SpaceParams sp, int64_t n_jobs, const unsigned* __restrict__ wmm,
-                              float* __restrict__ fast) {
+// n_jobs) gets A = B = -1e30 (infeasible) and W = 0. A warp owns one row
+// (lanes = the 20 configs of the stage) and reads the row-major ka/kb/w rows
+// written by k_project_all.
+__global__ void __launch_bounds__(256) k_gather_fast(const float* __restrict__ ka, const float* __restrict__ kb,
+                                                     const float* __restrict__ w, const SpaceParams sp,
+                                                     int64_t n_jobs, const unsigned long long* __restrict__ err,
+                                                     const unsigned* __restrict__ wmm, float* __restrict__ fast) {
   __shared__ float s_lo[kMaxSlots];
   __shared__ float s_inv;
   if (threadIdx.x == 0) {
@@ -194,64 +204,60 @@ __global__ void k_gather_fast(const float* __restrict__ ka, const float* __restr
     s_inv = span > 0.0f ? (float)(33554430 - sp.n_slots) / span : 0.0f;
   }
   __syncthreads();
-  const int64_t total = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad * kStageRS;
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int col = (int)(idx % kStageRS);
-  int64_t r = idx / kStageRS;
-  const int64_t job = r % sp.n_jobs_pad;
-  r /= sp.n_jobs_pad;
-  const int stage = (int)(r % sp.n_stages);
-  const int role = (int)(r / sp.n_stages);
-  const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
-  const int c = stage * kStageCfg + col;
-  const bool pad = col >= kStageCfg || c >= sp.n_cfg || job >= n_jobs;
-  float v;
-  if (kind == sp.n_slots) {
-    unsigned bits = 0u;
-    if (!pad) {
-      const int s = c / sp.n_caps, p = c - (c / sp.n_caps) * sp.n_caps;
-      const float qf = rintf((w_row(w, sp, slot, s, job)[p] - s_lo[slot]) * s_inv);
-      bits = (qf > 0.0f ? (unsigned)qf : 0u) << 5;
-      if (slot == 0) bits += 0x00800000u;
-      if (slot == sp.n_slots - 1) bits |= (unsigned)(31 - col);
-    }
-    v = __uint_as_float(bits);
-  } else if (pad) {
-    v = -1e30f;
-  } else {
-    const int s = c / sp.n_caps, p = c - (c / sp.n_caps) * sp.n_caps;
-    if (kind == 0) {
-      v = ka_row(ka, sp, sp.slice[s][slot], job)[p];
+  if (*err != ~0ull) return;
+  const int col = threadIdx.x & 31;
+  if (col >= kStageRS) return;
+  const unsigned npad = (unsigned)sp.n_jobs_pad;
+  const unsigned rows = (unsigned)(sp.n_roles * sp.n_stages) * npad;
+  const unsigned wpb = blockDim.x >> 5;
+  for (unsigned r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    const unsigned job = r % npad, rs_ = r / npad;
+    const int stage = (int)(rs_ % sp.n_stages), role = (int)(rs_ / sp.n_stages);
+    const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
+    const int c = stage * kStageCfg + col;
+    const bool pad = col >= kStageCfg || c >= sp.n_cfg || job >= n_jobs;
+    float v;
+    if (kind == sp.n_slots) {
+      unsigned bits = 0u;
+      if (!pad) {
+        const int s = c / sp.n_caps, p = c - s * sp.n_caps;
+        const float qf = rintf((w_row(w, sp, slot, s, job)[p] - s_lo[slot]) * s_inv);
+        bits = (qf > 0.0f ? (unsigned)qf : 0u) << 5;
+        if (slot == 0) bits += 0x00800000u;
+        if (slot == sp.n_slots - 1) bits |= (unsigned)(31 - col);
+      }
+      v = __uint_as_float(bits);
+    } else if (pad) {
+      v = -1e30f;
     } else {
-      const int l = kind - 1 + (kind - 1 >= slot ? 1 : 0);  // the kind-th other slot, ascending
-      v = ka_row(kb, sp, sp.slice[s][l], job)[p];
+      const int s = c / sp.n_caps, p = c - s * sp.n_caps;
+      if (kind == 0) {
+        v = ka_row(ka, sp, sp.slice[s][slot], job)[p];
+      } else {
+        const int l = kind - 1 + (kind - 1 >= slot ? 1 : 0);  // the kind-th other slot, ascending
+        v = ka_row(kb, sp, sp.slice[s][l], job)[p];
+      }
     }
+    fast[(size_t)r * kStageRS + col] = v;
   }
-  fast[idx] = v;
+}
+
+__global__ void k_init_wmm(unsigned* wmm) {
+  if (threadIdx.x < 2 * kMaxSlots) wmm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
 }
 
 void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
                     const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
                     float* fast, unsigned* wmm, cudaStream_t st) {
-  int64_t total = (int64_t)sp.n_slices * sp.n_jobs_pad * sp.rs;
-  if (n_jobs <= 0 || total <= 0) return;
-  int bs = 256;
-  k_project<<<(unsigned)((total + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
-                                                               err, ka, kb);
-  int64_t tw = (int64_t)sp.n_slots * sp.n_states * sp.n_jobs_pad * sp.rs;
-  k_project_w<<<(unsigned)((tw + bs - 1) / bs), bs, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d,
-                                                              err, w);
-  unsigned init[2 * kMaxSlots];
-  for (int i = 0; i < kMaxSlots; i++) {
-    init[2 * i] = 0xFFFFFFFFu;
-    init[2 * i + 1] = 0u;
-  }
-  cudaMemcpyAsync(wmm, init, sizeof init, cudaMemcpyHostToDevice, st);
-  int64_t mb = std::min<int64_t>((tw / sp.n_slots + bs - 1) / bs, 148 * 4);
-  k_w_minmax<<<(unsigned)mb, bs, 0, st>>>(w, sp, n_jobs, wmm);
-  const int64_t tf = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad * kStageRS;
-  k_gather_fast<<<(unsigned)((tf + bs - 1) / bs), bs, 0, st>>>(ka, kb, w, sp, n_jobs, wmm, fast);
+  if (n_jobs <= 0) return;
+  k_init_wmm<<<1, 32, 0, st>>>(wmm);
+  const int64_t rows = ((int64_t)sp.n_slices + (int64_t)sp.n_slots * sp.n_states) * sp.n_jobs_pad;
+  int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  k_project_all<<<(unsigned)blocks, 256, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w,
+                                                   wmm);
+  const int64_t frows = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad;
+  blocks = std::min<int64_t>((frows + 7) / 8, 148 * 16);
+  k_gather_fast<<<(unsigned)blocks, 256, 0, st>>>(ka, kb, w, sp, n_jobs, err, wmm, fast);
 }
 
 // ---------------------------------------------------------------------------
