@@ -85,71 +85,132 @@ __global__ void k_keys_in_range(const float* __restrict__ obj, int64_t first, in
   }
 }
 
+// The sequential rule over a sorted window of 1024 candidates, resolved in
+// parallel: an undecided candidate whose jobs are all still free and that is
+// the lowest-index undecided candidate on every one of its jobs cannot be
+// blocked by any earlier candidate, so it is taken; candidates touching a job
+// just taken are dropped; repeat until the window is decided. The taken set is
+// exactly the sequential greedy's, and picks are emitted in window (key) order.
 template <int NS>
 __global__ void __launch_bounds__(1024, 1)
     k_greedy_scan(const unsigned long long* __restrict__ sorted, int64_t m, int64_t n_jobs, uint32_t* taken_g,
                   unsigned long long* picks, int64_t* n_picks, int64_t k_max) {
-  extern __shared__ uint32_t s_taken[];  // n_jobs bits
-  __shared__ int32_t s_job[1024][NS];
-  __shared__ uint32_t s_flag[32];
+  constexpr int CPT = 4;            // candidates per thread: window = 4096 keys
+  constexpr int WIN = 1024 * CPT;
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_taken = s_dyn;                                                    // n_jobs bits
+  int32_t* s_first = reinterpret_cast<int32_t*>(s_dyn + ((n_jobs + 31) >> 5));  // n_jobs
+  __shared__ int32_t s_wsum[32];
   __shared__ int64_t s_np;
   const int words = (int)((n_jobs + 31) >> 5);
   for (int i = threadIdx.x; i < words; i += blockDim.x) s_taken[i] = taken_g[i];
+  for (int i = threadIdx.x; i < n_jobs; i += blockDim.x) s_first[i] = 0x7FFFFFFF;
   if (threadIdx.x == 0) s_np = *n_picks;
   __syncthreads();
-  for (int64_t base = 0; base < m; base += 1024) {
+  const int t = threadIdx.x;
+  unsigned long long nxt[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; u++) {
+    const int64_t i = (int64_t)t * CPT + u;
+    nxt[u] = i < m ? sorted[i] : 0ull;
+  }
+  for (int64_t base = 0; base < m; base += WIN) {
     if (s_np >= k_max) break;
-    const int64_t i = base + threadIdx.x;
-    bool fr = false;
-    if (i < m) {
-      const unsigned long long key = sorted[i];
-      if (key) {
-        const int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+    unsigned long long key[CPT];
+    int32_t jb[CPT][3];
+    bool und[CPT], acc[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; u++) {
+      key[u] = nxt[u];
+      const int64_t i2 = base + WIN + (int64_t)t * CPT + u;  // prefetch the next window
+      nxt[u] = i2 < m ? sorted[i2] : 0ull;
+      acc[u] = false;
+      und[u] = false;
+      jb[u][0] = jb[u][1] = jb[u][2] = 0;
+      if (key[u]) {
+        const int64_t sid = (int64_t)(0xFFFFFFFFull - (key[u] & 0xFFFFFFFFull));
         int64_t j[3];
         unrank_set<NS>(sid, j);
-        fr = true;
+        und[u] = true;
 #pragma unroll
         for (int q = 0; q < NS; q++) {
-          s_job[threadIdx.x][q] = (int32_t)j[q];
-          fr = fr && !((s_taken[j[q] >> 5] >> (j[q] & 31)) & 1u);
+          jb[u][q] = (int32_t)j[q];
+          und[u] = und[u] && !((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u);
         }
       }
     }
-    const unsigned bal = __ballot_sync(0xFFFFFFFFu, fr);
-    if ((threadIdx.x & 31) == 0) s_flag[threadIdx.x >> 5] = bal;
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < CPT; u++) any = any || und[u];
+    while (__syncthreads_or(any)) {
+#pragma unroll
+      for (int u = 0; u < CPT; u++)
+        if (und[u])
+#pragma unroll
+          for (int q = 0; q < NS; q++) atomicMin(&s_first[jb[u][q]], t * CPT + u);
+      __syncthreads();
+      bool take[CPT];
+#pragma unroll
+      for (int u = 0; u < CPT; u++) {
+        take[u] = und[u];
+        if (und[u])
+#pragma unroll
+          for (int q = 0; q < NS; q++) take[u] = take[u] && (s_first[jb[u][q]] == t * CPT + u);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < CPT; u++) {
+        if (und[u])
+#pragma unroll
+          for (int q = 0; q < NS; q++) s_first[jb[u][q]] = 0x7FFFFFFF;  // reset for the next round
+        if (take[u]) {
+#pragma unroll
+          for (int q = 0; q < NS; q++) atomicOr(&s_taken[jb[u][q] >> 5], 1u << (jb[u][q] & 31));
+          acc[u] = true;
+          und[u] = false;
+        }
+      }
+      __syncthreads();
+      any = false;
+#pragma unroll
+      for (int u = 0; u < CPT; u++) {
+        if (und[u])
+#pragma unroll
+          for (int q = 0; q < NS; q++)
+            if ((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u) und[u] = false;
+        any = any || und[u];
+      }
+    }
+    // emit the window's picks in index order (block prefix sum), stopping at k_max
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < CPT; u++) cnt += acc[u];
+    int incl = cnt;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+      if ((t & 31) >= off) incl += v;
+    }
+    if ((t & 31) == 31) s_wsum[t >> 5] = incl;
     __syncthreads();
-    if (threadIdx.x < 32) {
-      // one warp applies the sequential rule to the window's free candidates, in order
-      int64_t np = s_np;
-      for (int w = 0; w < 32 && np < k_max; w++) {
-        unsigned mask = s_flag[w];
-        while (mask && np < k_max) {
-          const int b = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const int t = w * 32 + b;
-          bool ok = true;
-#pragma unroll
-          for (int q = 0; q < NS; q++) {
-            const int jj = s_job[t][q];
-            ok = ok && !((s_taken[jj >> 5] >> (jj & 31)) & 1u);
-          }
-          if (ok) {
-            __syncwarp();
-            if (threadIdx.x == 0) {
-#pragma unroll
-              for (int q = 0; q < NS; q++) {
-                const int jj = s_job[t][q];
-                s_taken[jj >> 5] |= 1u << (jj & 31);
-              }
-              picks[np] = sorted[base + t];
-            }
-            __syncwarp();
-            np++;
-          }
-        }
+    if (t < 32) {
+      int v = s_wsum[t];
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u2 = __shfl_up_sync(0xFFFFFFFFu, v, off);
+        if (t >= off) v += u2;
       }
-      if (threadIdx.x == 0) s_np = np;
+      s_wsum[t] = v;  // inclusive over warps
     }
+    __syncthreads();
+    const int64_t np0 = s_np;
+    int rank = (t >= 32 ? s_wsum[(t >> 5) - 1] : 0) + incl - cnt;
+#pragma unroll
+    for (int u = 0; u < CPT; u++)
+      if (acc[u]) {
+        if (np0 + rank < k_max) picks[np0 + rank] = key[u];
+        rank++;
+      }
+    __syncthreads();
+    if (t == 0) s_np = (np0 + s_wsum[31] < k_max) ? np0 + s_wsum[31] : k_max;
     __syncthreads();
   }
   for (int i = threadIdx.x; i < words; i += blockDim.x) taken_g[i] = s_taken[i];
@@ -231,7 +292,7 @@ cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long lo
 cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
                                uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
                                cudaStream_t st) {
-  const size_t smem = (size_t)((n_jobs + 31) / 32) * 4;
+  const size_t smem = (size_t)((n_jobs + 31) / 32) * 4 + (size_t)n_jobs * 4;
   if (n_slots == 2) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_greedy_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_greedy_scan<2><<<1, 1024, smem, st>>>(sorted, m, n_jobs, taken_bits, picks, n_picks, k_max);
