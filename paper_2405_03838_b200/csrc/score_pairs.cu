@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   int64_t I, J;
   tile_coords(g, t, &I, &J);
   int s = 0, buf = 0;
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit b = parity of the next wait on bars[b]
   if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
 
   float breg[kM][kM];
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const bool has_next = nt < g.n_tiles;
     if (has_next && threadIdx.x == 0)
       issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
-    mbar_wait(&bars[buf], phase[buf]);
-    phase[buf] ^= 1u;
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
 
     const float4* st4 = reinterpret_cast<const float4*>(smem + buf * stage_floats);
     const int blk4 = kTile * rs4;
@@ -201,48 +201,78 @@ __global__ void __launch_bounds__(kThreads, MINB)
           breg[a][b] = 0.0f;
         }
       __syncthreads();
-#pragma unroll 2
-      for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
-        const int rj = e >> 6, ri = e & 63;
-        const int64_t j0 = I * kTile + ri;
-        const int64_t j1 = J * kTile + rj;
-        const int sg = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
-        const unsigned kbits = __float_as_uint(sbest[rj * kBgRow + ri]);
-        sbg[rj * kBgRow + ri] = -1;
-        if (!(j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1)) continue;
-        float bo = -INFINITY;
-        int bc = -1;
-        if (sg >= 0) {
-          // the config: stage sg, offset from the key's low bits; evaluate it exactly
-          int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
-          int64_t jj[2] = {j0, j1};
-          float r[2], o;
-          if (c < sp.n_cfg) {
-            eval_cfg<2>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
-            if (r[0] > 0.0f && r[1] > 0.0f) {
-              bo = o;
-              bc = c;
-            }
+      // 8 pairs per pass with all their loads in flight: the packed keys of the
+      // decoded config (fast W0/W1 rows) must reproduce the stored key -- then the
+      // config is the stage argmax and feasible (the key was not clipped), and its
+      // exact FP32 objective is w0 + w1; otherwise (a margin below obj/2^40)
+      // the stage is scanned exactly.
+      constexpr int kPass = 8;
+#pragma unroll 1
+      for (int e0 = 0; e0 < kTile * kTile; e0 += kPass * kThreads) {
+        unsigned kb_[kPass], q0[kPass], q1[kPass];
+        float f0[kPass], f1[kPass];
+        int c_[kPass], sg_[kPass];
+        bool ok_[kPass];
+#pragma unroll
+        for (int u = 0; u < kPass; u++) {
+          const int e = e0 + u * kThreads + threadIdx.x;
+          const int rj = e >> 6, ri = e & 63;
+          const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+          const int sg = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
+          kb_[u] = __float_as_uint(sbest[rj * kBgRow + ri]);
+          sbg[rj * kBgRow + ri] = -1;
+          ok_[u] = j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1;
+          sg_[u] = ok_[u] ? sg : -1;
+          const int off = 31 - (int)(kb_[u] & 31u);
+          const int c = sg * kStageCfg + off;
+          c_[u] = c;
+          q0[u] = q1[u] = 0u;
+          f0[u] = f1[u] = 0.0f;
+          if (sg_[u] >= 0 && off < kStageCfg && c < sp.n_cfg) {
+            const float* rw0 = fast + (((int64_t)2 * sp.n_stages + sg) * sp.n_jobs_pad + j0) * kStageRS;
+            const float* rw1 = fast + (((int64_t)5 * sp.n_stages + sg) * sp.n_jobs_pad + j1) * kStageRS;
+            const int st = c / sp.n_caps, p = c - st * sp.n_caps;
+            q0[u] = __float_as_uint(__ldg(rw0 + off));
+            q1[u] = __float_as_uint(__ldg(rw1 + off));
+            f0[u] = __ldg(w_row(w, sp, 0, st, j0) + p);
+            f1[u] = __ldg(w_row(w, sp, 1, st, j1) + p);
           }
-          if (bc < 0) {
-            // the key was clipped by a margin below obj/2^40: exact scan of the stage
-            const int cend = min(sg * kStageCfg + kStageCfg, sp.n_cfg);
-            for (c = sg * kStageCfg; c < cend; c++) {
-              eval_cfg<2>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
-              if (r[0] > 0.0f && r[1] > 0.0f && o > bo) {
-                bo = o;
-                bc = c;
+        }
+#pragma unroll
+        for (int u = 0; u < kPass; u++) {
+          if (!ok_[u]) continue;
+          const int e = e0 + u * kThreads + threadIdx.x;
+          const int rj = e >> 6, ri = e & 63;
+          const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+          float bo = -INFINITY;
+          int bc = -1;
+          if (sg_[u] >= 0) {
+            if (q0[u] + q1[u] == kb_[u] && (kb_[u] & 31u) >= 32u - kStageCfg) {
+              bo = __fadd_rn(f0[u], f1[u]);
+              bc = c_[u];
+            } else {
+              // the key was clipped by a fairness margin below obj/2^40: exact scan
+              const int sg = sg_[u];
+              const int cend = min(sg * kStageCfg + kStageCfg, sp.n_cfg);
+              int64_t jj[2] = {j0, j1};
+              float r[2], o;
+              for (int c = sg * kStageCfg; c < cend; c++) {
+                eval_cfg<2>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
+                if (r[0] > 0.0f && r[1] > 0.0f && o > bo) {
+                  bo = o;
+                  bc = c;
+                }
               }
             }
           }
-        }
-        const int64_t sid = j1 * (j1 - 1) / 2 + j0;
-        const int64_t k = sid - g.first_set;
-        if (out_obj) out_obj[k] = bo;
-        if (out_cfg) out_cfg[k] = bc;
-        if (bc >= 0) {
-          const unsigned long long kk = pack_key(bo, sid);
-          key = kk > key ? kk : key;
+          const int64_t sid = j1 * (j1 - 1) / 2 + j0;
+          const int64_t k = sid - g.first_set;
+          if (out_obj) out_obj[k] = bo;
+          if (out_cfg) out_cfg[k] = bc;
+          if (bc >= 0) {
+            const unsigned long long kk = pack_key(bo, sid);
+            key = kk > key ? kk : key;
+          }
         }
       }
     }
