@@ -105,7 +105,11 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
   constexpr int stage_floats = 8 * kTT * rs + 4 * rs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx = ((warp & 3) << 2) | (lane & 3), ty = ((warp >> 2) << 3) | (lane >> 2);
+  // lane bits: a quad (4 consecutive lanes) spans 2 values of tx and 2 of ty, so
+  // every LDS.128 of an operand row costs 2 shared wavefronts (4 when a quad
+  // reads 4 different rows: tools/microbench/lds.cu)
+  const int tx = ((warp & 3) << 2) | (((lane >> 2) & 1) << 1) | (lane & 1);
+  const int ty = ((warp >> 2) << 3) | ((lane >> 3) << 1) | ((lane >> 1) & 1);
   const unsigned one = g.one;
   unsigned long long key = 0;
 
