@@ -51,6 +51,8 @@ struct PairGrid {
   int64_t base;       // tiles before the first column tile: jt0*(jt0+1)/2
   int64_t first_set;  // output index offset
   unsigned one;       // runtime 1: keeps the integer adds on the FMA pipe (IMAD)
+  int dbg;            // COSCHED_PAIR_DEBUG (timing experiments only, wrong results): bit 0 skips
+                      // the tile end, bit 1 the TMA stage loads, bit 2 the per-stage barrier
 };
 
 __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_t* I, int64_t* J) {
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   tile_coords(g, t, &I, &J);
   int s = 0, buf = 0;
   unsigned phase = 0u;  // bit b = parity of the next wait on bars[b]
-  if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
+  if (threadIdx.x == 0 && !(g.dbg & 2)) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
 
   float breg[kM][kM];
 #pragma unroll
@@ -138,10 +140,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (nt < g.n_tiles) tile_coords(g, nt, &nI, &nJ);
     }
     const bool has_next = nt < g.n_tiles;
-    if (has_next && threadIdx.x == 0)
-      issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
-    mbar_wait(&bars[buf], (phase >> buf) & 1u);
-    phase ^= 1u << buf;
+    if (!(g.dbg & 2)) {
+      if (has_next && threadIdx.x == 0)
+        issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    }
 
     const float4* st4 = reinterpret_cast<const float4*>(smem + buf * stage_floats);
     const int blk4 = kTile * rs4;
@@ -193,7 +197,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
           sbg[(ty + 16 * b) * kBgRow + tx + 16 * a] = (int16_t)s;
         }
 
-    if (s == sp.n_stages - 1) {
+    if (s == sp.n_stages - 1 && (g.dbg & 1)) {
+#pragma unroll
+      for (int a = 0; a < kM; a++)
+#pragma unroll
+        for (int b = 0; b < kM; b++) {
+          key = max(key, (unsigned long long)__float_as_uint(breg[a][b]));
+          breg[a][b] = 0.0f;
+        }
+    } else if (s == sp.n_stages - 1) {
       // ---- tile end: park each pair's best key, then resolve and write with a
       // rolled loop in which a warp owns 32 consecutive j0 of one column
       // (128-byte coalesced obj/cfg writes)
@@ -281,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
 
-    __syncthreads();  // everyone is done with `buf` (and the per-pair state) before reuse
+    if (!(g.dbg & 4)) __syncthreads();  // everyone is done with `buf` (and the per-pair state) before reuse
     if (!has_next) break;
     t = nt;
     I = nI;
@@ -315,6 +327,12 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   g.c1 = c1;
   g.first_set = first;
   g.one = 1u;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("COSCHED_PAIR_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  g.dbg = dbg;
   int64_t jt0 = c0 / kTile, jt1 = (c1 - 1) / kTile;
   g.base = jt0 * (jt0 + 1) / 2;
   g.n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - g.base;
