@@ -23,11 +23,18 @@ constexpr int kStageCfg = 20;
 constexpr int kStageRS = 20;
 
 // Feasibility scale: the projection stores
-// K*(U - alpha) and K*V, so a slot's margin r - alpha appears as
-// r'' = K*(r - alpha), exactly (K is a power of two), and the masked objective
-// min3(obj, r0'', r1'') equals obj unless a margin is below obj/K (< 1e-11).
-constexpr float kScale = 1099511627776.0f;  // 2^40
-constexpr float kInvScale = 1.0f / 1099511627776.0f;
+// K*fl(U - alpha) and K*V with K = 2^80 (exact power-of-two scaling), each
+// flushed to 0 when its magnitude is below K*2^-54 = 2^26 (a change of
+// < 5.6e-17 in RPerf). Every nonzero operand is then a multiple of 8 (its ulp
+// is >= 2^3), so every sum of them -- a fairness margin r'' = K*(RPerf - alpha)
+// in the canonical order -- is 0, negative, or >= 8. The packed objective of
+// the tiled scorers is a float < 4.0, so the masked key min3(obj, r0'', r1'')
+// is the objective exactly when every margin is positive and <= 0 otherwise.
+constexpr float kScale = 1208925819614629174706176.0f;       // 2^80
+constexpr float kInvScale = 8.2718061255302767e-25f;         // 2^-80
+constexpr float kFlushBelow = 67108864.0f;                   // 2^26 (scaled units)
+constexpr float kClampAbs = 8.5070591730234616e37f;          // 2^126: sums of three stay finite
+constexpr float kPadMargin = -3.4028234663852886e38f;        // -FLT_MAX: padding caps/jobs, infeasible
 
 // Everything a scoring kernel needs about the search space, passed by value
 // (kernel parameter space -> constant bank, read with c[0x0][...] operands).
@@ -56,8 +63,8 @@ struct DeviceTables {
 
 // Workspace layout (carved from the caller's buffer, all 256-byte aligned).
 struct Workspace {
-  float* ka = nullptr;              // [n_slices][n_jobs_pad][rs] = K*(U - alpha); padding = -1e30
-  float* kb = nullptr;              // [n_slices][n_jobs_pad][rs] = K*V;           padding = -1e30
+  float* ka = nullptr;              // [n_slices][n_jobs_pad][rs] = K*(U - alpha) (flushed/clamped); padding = -FLT_MAX
+  float* kb = nullptr;              // [n_slices][n_jobs_pad][rs] = K*V (flushed/clamped);       padding = -FLT_MAX
   float* w = nullptr;               // [n_slots][n_states][n_jobs_pad][rs] throughput share of the job in
                                     //   slot i of state s at cap p, already divided by P (Problem 2):
                                     //   (U[s_i] + sum_{l != i} V[s_l]) * invP; padding = -1e30

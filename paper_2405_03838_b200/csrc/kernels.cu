@@ -59,7 +59,7 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
 // a2 + a3: basis and projection. Thread per (job, slice, padded cap):
 //   U = C[p][s] . H(F_n),  V = D[p][s] . J(F_n)   (the two dot products of P:L458)
 //   ka = K*(U - alpha),   kb = K*V               (exact power-of-two scaling)
-// Padding caps (p >= n_caps) get -1e30 so every candidate using them is infeasible.
+// Padding caps (p >= n_caps) get kPadMargin (-FLT_MAX) so every candidate using them is infeasible.
 __device__ __forceinline__ float dot_u(const float* __restrict__ C, const float h[6]) {
   float u = __fmul_rn(C[0], h[0]);
 #pragma unroll
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F
         const unsigned s = r / npad, n = r - s * npad;
         const size_t o = (size_t)r * sp.rs + p;
         if (p >= sp.n_caps || n >= n_jobs) {
-          ka[o] = -1e30f;
-          kb[o] = -1e30f;
+          ka[o] = kPadMargin;
+          kb[o] = kPadMargin;
           continue;
         }
         const int64_t row = jobs ? (int64_t)jobs[n] : (int64_t)n;
@@ -128,8 +128,12 @@ __global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F
         basis_hj(F + row * 8, h, j);
         const float u = dot_u(coef_c + ((int64_t)p * sp.n_slices + s) * 6, h);
         const float v = dot_v(coef_d + ((int64_t)p * sp.n_slices + s) * 3, j);
-        ka[o] = __fmul_rn(__fsub_rn(u, sp.alpha), kScale);
-        kb[o] = __fmul_rn(v, kScale);
+        // cosched_internal.h: flushed (margins are 0 or >= 8) and clamped to
+        // +-2^126 (no overflow in a sum of three, no NaN against the padding)
+        const float sa = fminf(fmaxf(__fmul_rn(__fsub_rn(u, sp.alpha), kScale), -kClampAbs), kClampAbs);
+        const float sb = fminf(fmaxf(__fmul_rn(v, kScale), -kClampAbs), kClampAbs);
+        ka[o] = fabsf(sa) < kFlushBelow ? 0.0f : sa;
+        kb[o] = fabsf(sb) < kFlushBelow ? 0.0f : sb;
       } else {
         const unsigned rw = r - rows_k;
         const unsigned n = rw % npad, ss = rw / npad;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F
 //     objective up to one quantum per slot (< 4e-7 relative for the presets)
 //     and carries the config's offset in its stage in the low 5 bits.
 // Rows are [role][stage][job][kStageRS]; padding (configs >= n_cfg, jobs >=
-// n_jobs) gets A = B = -1e30 (infeasible) and W = 0. A warp owns one row
+// n_jobs) gets A = B = kPadMargin (infeasible) and W = 0. A warp owns one row
 // (lanes = the 20 configs of the stage) and reads the row-major ka/kb/w rows
 // written by k_project_all.
 __global__ void __launch_bounds__(256) k_gather_fast(const float* __restrict__ ka, const float* __restrict__ kb,
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(256) k_gather_fast(const float* __restrict__ k
       }
       v = __uint_as_float(bits);
     } else if (pad) {
-      v = -1e30f;
+      v = kPadMargin;
     } else {
       const int s = c / sp.n_caps, p = c - s * sp.n_caps;
       if (kind == 0) {

@@ -10,7 +10,7 @@
 // and the per-pair argmax of x: configs are walked in stages of 24
 // along the flattened axis c = state * n_caps + cap (no cap padding); the stage
 // of the best x is kept per pair, its offset comes back from x's low bits, and
-// the winner is re-evaluated exactly in FP32 at tile end.
+// the winner's exact FP32 objective is read back at tile end.
 //
 // Design (DESIGN.md §5 "Pair scorer"):
 //  - persistent CTAs (two per SM, 16 warps, 128 registers per thread) walk 64x64
@@ -24,8 +24,8 @@
 //    4 FMNMX3 (masked objective) + 2 FMNMX3 (running max): ALU 1.5 per
 //    candidate, FMA pipe 2 -- the mix that measured fastest in
 //    tools/microbench/inner.cu;
-//  - per stage and pair one FSETP + 2 predicated moves; per tile and pair one
-//    exact FP32 re-evaluation of the chosen config.
+//  - per stage and pair one FSETP + 2 predicated moves; per tile and pair the
+//    exact FP32 objective of the chosen config (2 loads + 1 FADD).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -51,8 +51,6 @@ struct PairGrid {
   int64_t base;       // tiles before the first column tile: jt0*(jt0+1)/2
   int64_t first_set;  // output index offset
   unsigned one;       // runtime 1: keeps the integer adds on the FMA pipe (IMAD)
-  int dbg;            // COSCHED_PAIR_DEBUG (timing experiments only, wrong results): bit 0 skips
-                      // the tile end, bit 1 the TMA stage loads, bit 2 the per-stage barrier
 };
 
 __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_t* I, int64_t* J) {
@@ -84,8 +82,8 @@ __device__ __forceinline__ void issue_stage(float* stage, uint64_t* bar, const S
 
 template <int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ ka,
-                        const float* __restrict__ kb, const float* __restrict__ w, const float* __restrict__ fast,
+    k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
+                        const float* __restrict__ fast,
                         float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
                         unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err) {
   extern __shared__ __align__(128) float smem[];
@@ -122,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   tile_coords(g, t, &I, &J);
   int s = 0, buf = 0;
   unsigned phase = 0u;  // bit b = parity of the next wait on bars[b]
-  if (threadIdx.x == 0 && !(g.dbg & 2)) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
+  if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
 
   float breg[kM][kM];
 #pragma unroll
@@ -140,12 +138,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (nt < g.n_tiles) tile_coords(g, nt, &nI, &nJ);
     }
     const bool has_next = nt < g.n_tiles;
-    if (!(g.dbg & 2)) {
-      if (has_next && threadIdx.x == 0)
-        issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
-      mbar_wait(&bars[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-    }
+    if (has_next && threadIdx.x == 0)
+      issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
 
     const float4* st4 = reinterpret_cast<const float4*>(smem + buf * stage_floats);
     const int blk4 = kTile * rs4;
@@ -197,15 +193,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           sbg[(ty + 16 * b) * kBgRow + tx + 16 * a] = (int16_t)s;
         }
 
-    if (s == sp.n_stages - 1 && (g.dbg & 1)) {
-#pragma unroll
-      for (int a = 0; a < kM; a++)
-#pragma unroll
-        for (int b = 0; b < kM; b++) {
-          key = max(key, (unsigned long long)__float_as_uint(breg[a][b]));
-          breg[a][b] = 0.0f;
-        }
-    } else if (s == sp.n_stages - 1) {
+    if (s == sp.n_stages - 1) {
       // ---- tile end: park each pair's best key, then resolve and write with a
       // rolled loop in which a warp owns 32 consecutive j0 of one column
       // (128-byte coalesced obj/cfg writes)
@@ -217,70 +205,42 @@ __global__ void __launch_bounds__(kThreads, MINB)
           breg[a][b] = 0.0f;
         }
       __syncthreads();
-      // 8 pairs per pass with all their loads in flight: the packed keys of the
-      // decoded config (fast W0/W1 rows) must reproduce the stored key -- then the
-      // config is the stage argmax and feasible (the key was not clipped), and its
-      // exact FP32 objective is w0 + w1; otherwise (a margin below obj/2^40)
-      // the stage is scanned exactly.
+      // 8 pairs per pass with all their loads in flight. A positive fairness
+      // margin is >= 8 (kScale, cosched_internal.h) and a packed key is < 4.0, so
+      // the best masked key of a feasible pair is never clipped: its low bits
+      // are the stage offset of the argmax, and the reported objective is the
+      // exact FP32 w0 + w1 of that config (2 loads).
       constexpr int kPass = 8;
 #pragma unroll 1
       for (int e0 = 0; e0 < kTile * kTile; e0 += kPass * kThreads) {
-        unsigned kb_[kPass], q0[kPass], q1[kPass];
         float f0[kPass], f1[kPass];
-        int c_[kPass], sg_[kPass];
-        bool ok_[kPass];
+        int c_[kPass];
 #pragma unroll
         for (int u = 0; u < kPass; u++) {
           const int e = e0 + u * kThreads + threadIdx.x;
           const int rj = e >> 6, ri = e & 63;
           const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
           const int sg = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
-          kb_[u] = __float_as_uint(sbest[rj * kBgRow + ri]);
+          const unsigned kbits = __float_as_uint(sbest[rj * kBgRow + ri]);
           sbg[rj * kBgRow + ri] = -1;
-          ok_[u] = j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1;
-          sg_[u] = ok_[u] ? sg : -1;
-          const int off = 31 - (int)(kb_[u] & 31u);
-          const int c = sg * kStageCfg + off;
-          c_[u] = c;
-          q0[u] = q1[u] = 0u;
+          const bool ok = j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1;
+          const int c = sg * kStageCfg + 31 - (int)(kbits & 31u);
+          c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
           f0[u] = f1[u] = 0.0f;
-          if (sg_[u] >= 0 && off < kStageCfg && c < sp.n_cfg) {
-            const float* rw0 = fast + (((int64_t)2 * sp.n_stages + sg) * sp.n_jobs_pad + j0) * kStageRS;
-            const float* rw1 = fast + (((int64_t)5 * sp.n_stages + sg) * sp.n_jobs_pad + j1) * kStageRS;
+          if (c_[u] >= 0) {
             const int st = c / sp.n_caps, p = c - st * sp.n_caps;
-            q0[u] = __float_as_uint(__ldg(rw0 + off));
-            q1[u] = __float_as_uint(__ldg(rw1 + off));
             f0[u] = __ldg(w_row(w, sp, 0, st, j0) + p);
             f1[u] = __ldg(w_row(w, sp, 1, st, j1) + p);
           }
         }
 #pragma unroll
         for (int u = 0; u < kPass; u++) {
-          if (!ok_[u]) continue;
+          if (c_[u] == -2) continue;
           const int e = e0 + u * kThreads + threadIdx.x;
-          const int rj = e >> 6, ri = e & 63;
+          const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0 of one column
           const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
-          float bo = -INFINITY;
-          int bc = -1;
-          if (sg_[u] >= 0) {
-            if (q0[u] + q1[u] == kb_[u] && (kb_[u] & 31u) >= 32u - kStageCfg) {
-              bo = __fadd_rn(f0[u], f1[u]);
-              bc = c_[u];
-            } else {
-              // the key was clipped by a fairness margin below obj/2^40: exact scan
-              const int sg = sg_[u];
-              const int cend = min(sg * kStageCfg + kStageCfg, sp.n_cfg);
-              int64_t jj[2] = {j0, j1};
-              float r[2], o;
-              for (int c = sg * kStageCfg; c < cend; c++) {
-                eval_cfg<2>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
-                if (r[0] > 0.0f && r[1] > 0.0f && o > bo) {
-                  bo = o;
-                  bc = c;
-                }
-              }
-            }
-          }
+          const int bc = c_[u];
+          const float bo = bc >= 0 ? __fadd_rn(f0[u], f1[u]) : -INFINITY;
           const int64_t sid = j1 * (j1 - 1) / 2 + j0;
           const int64_t k = sid - g.first_set;
           if (out_obj) out_obj[k] = bo;
@@ -293,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
 
-    if (!(g.dbg & 4)) __syncthreads();  // everyone is done with `buf` (and the per-pair state) before reuse
+    __syncthreads();  // everyone is done with `buf` (and the per-pair state) before reuse
     if (!has_next) break;
     t = nt;
     I = nI;
@@ -318,7 +278,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     return c;
   };
   int64_t c0 = col_at(first), c1 = col_at(first + count);
-  if (c2(c0) != first || c2(c1) != first + count || c1 > n_jobs) {
+  if (c2(c0) != first || c2(c1) != first + count || c1 > n_jobs || (n_jobs + kTile - 1) / kTile >= 32768) {
     return launch_score(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, 0, st);
   }
   PairGrid g;
@@ -327,12 +287,6 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   g.c1 = c1;
   g.first_set = first;
   g.one = 1u;
-  static int dbg = -1;
-  if (dbg < 0) {
-    const char* e = getenv("COSCHED_PAIR_DEBUG");
-    dbg = e ? atoi(e) : 0;
-  }
-  g.dbg = dbg;
   int64_t jt0 = c0 / kTile, jt1 = (c1 - 1) / kTile;
   g.base = jt0 * (jt0 + 1) / 2;
   g.n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - g.base;
@@ -358,9 +312,9 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   if (grid > g.n_tiles) grid = g.n_tiles;
   if (grid < 1) grid = 1;
   if (minb == 1)
-    k_score_pairs_tiled<1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+    k_score_pairs_tiled<1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   else
-    k_score_pairs_tiled<2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+    k_score_pairs_tiled<2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   return 1;
 }
 

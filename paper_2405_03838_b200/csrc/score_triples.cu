@@ -19,7 +19,7 @@
 // [A0 B01 B02 W0 | A1 B10 B12 W1 | A2 B20 B21 W2]); per stage 8 role blocks of
 // 64 rows and 4 single j2 rows land by TMA bulk copies, double buffered. The
 // stage of each triple's best key is tracked; the offset comes back from the
-// key's low bits and the winner is re-evaluated exactly at tile end.
+// key's low bits and the winner's exact FP32 objective is read back at tile end.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -240,29 +240,18 @@ __global__ void __launch_bounds__(kTThreads, MINB)
         const unsigned kbits = __float_as_uint(sbest[rj * kTBgRow + ri]);
         sbg[rj * kTBgRow + ri] = -1;
         if (!(j0 < j1 && j1 < j2 && j2 < g.n_jobs && j2 >= g.c0 && j2 < g.c1)) continue;
+        // never clipped (positive margins >= 8 > packed key, cosched_internal.h):
+        // the key's low bits give the argmax config; its exact FP32 objective
+        // in the canonical order w0 + (w1 + w2)
         float bo = -INFINITY;
         int bc = -1;
-        if (sg >= 0) {
-          int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
-          int64_t jj[3] = {j0, j1, j2};
-          float r[3], o;
-          if (c < sp.n_cfg) {
-            eval_cfg<3>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
-            if (r[0] > 0.0f && r[1] > 0.0f && r[2] > 0.0f) {
-              bo = o;
-              bc = c;
-            }
-          }
-          if (bc < 0) {  // clipped key: exact scan of the stage
-            const int cend = min(sg * kStageCfg + kStageCfg, sp.n_cfg);
-            for (c = sg * kStageCfg; c < cend; c++) {
-              eval_cfg<3>(sp, ka, kb, w, jj, c / sp.n_caps, c % sp.n_caps, r, &o);
-              if (r[0] > 0.0f && r[1] > 0.0f && r[2] > 0.0f && o > bo) {
-                bo = o;
-                bc = c;
-              }
-            }
-          }
+        const int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
+        if (sg >= 0 && c < sp.n_cfg) {
+          const int st = c / sp.n_caps, p = c - st * sp.n_caps;
+          const float w0 = __ldg(w_row(w, sp, 0, st, j0) + p), w1 = __ldg(w_row(w, sp, 1, st, j1) + p),
+                      w2 = __ldg(w_row(w, sp, 2, st, j2) + p);
+          bo = __fadd_rn(w0, __fadd_rn(w1, w2));
+          bc = c;
         }
         const int64_t sid = j2 * (j2 - 1) * (j2 - 2) / 6 + j1 * (j1 - 1) / 2 + j0;
         const int64_t k = sid - g.first_set;

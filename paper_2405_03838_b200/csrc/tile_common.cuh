@@ -69,6 +69,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// 4-byte asynchronous gather global -> shared (LDGSTS): no register holds the
+// value while it is in flight; the issuing thread waits with cp_async_wait_all.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 
 }  // namespace
