@@ -150,6 +150,7 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.ka = (float*)take(proj);
   w.kb = (float*)take(proj);
   w.w = (float*)take(jp * n_slots * n_states * rs * sizeof(float));
+  w.hj = (float*)take(jp * 12 * sizeof(float));
   w.fast = (float*)take(jp * sp.n_roles * sp.n_stages * kStageRS * sizeof(float));
   w.wmm = (unsigned*)take(2 * kMaxSlots * sizeof(unsigned));
   w.best_key = (unsigned long long*)take(8);
@@ -550,8 +551,8 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   launch_fill_u64(ws.best_key, 0ull, 1, st);
   h->launches += 2;
   if (n_jobs > 0) {
-    launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, st);
-    launch_project(features_dev, jobs_dev, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
+    launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, ws.hj, st);
+    launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
     h->launches += 4;
   }
   cudaEventRecord(h->ev[1], st);

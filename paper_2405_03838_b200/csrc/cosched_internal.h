@@ -68,6 +68,7 @@ struct Workspace {
   float* w = nullptr;               // [n_slots][n_states][n_jobs_pad][rs] throughput share of the job in
                                     //   slot i of state s at cap p, already divided by P (Problem 2):
                                     //   (U[s_i] + sum_{l != i} V[s_l]) * invP; padding = -1e30
+  float* hj = nullptr;              // [n_jobs_pad][12] basis H1..H6, J1..J3 per queue position (k_validate)
   float* fast = nullptr;            // [n_roles][n_stages][n_jobs_pad][kStageRS] operands of the tiled scorers
                                     //   along the flattened config axis; the
                                     //   W roles hold fixed-point objective shares ("packed objective")
@@ -113,10 +114,10 @@ int64_t pad_jobs(int64_t n_jobs);
 
 // ---- kernel launchers (defined in kernels.cu) ------------------------------------
 void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
-                     unsigned long long* err, cudaStream_t st);
-void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
-                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
-                    float* fast, unsigned* wmm, cudaStream_t st);
+                     unsigned long long* err, float* hj, cudaStream_t st);
+void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
+                    const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
+                    cudaStream_t st);
 // Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
 // maxes the packed key into *best_key. Returns the number of kernels launched.
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,

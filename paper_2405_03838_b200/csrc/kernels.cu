@@ -20,11 +20,13 @@
 namespace cosched {
 
 // ---------------------------------------------------------------------------
-// a1: validation (SPEC.md L26-27 ranges, L54/L87 degenerate F1). One thread per
+// a1: validation (SPEC.md L26-27 ranges, L54/L87 degenerate F1) and a2: the
+// basis H, J of every queue position, computed once per job (4
+// IEEE divisions) into hj[pos][12] = (H1..H6, J1..J3, 0, 0, 0). One thread per
 // queue position; the first bad position wins through an atomicMin on
 // (pos << 8 | status).
 __global__ void k_validate(const float* __restrict__ F, int64_t n_rows, const int32_t* __restrict__ jobs,
-                           int64_t n_jobs, unsigned long long* err) {
+                           int64_t n_jobs, unsigned long long* err, float* __restrict__ hj) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= n_jobs) return;
   int64_t row = jobs ? (int64_t)jobs[q] : q;
@@ -44,134 +46,185 @@ __global__ void k_validate(const float* __restrict__ F, int64_t n_rows, const in
       if (!(tensor <= 100.0f)) code = COSCHED_E_RANGE;
       else if (!(v[0] > 0.01f)) code = COSCHED_E_DEGENERATE_PROFILE;
     }
+    if (!code) {
+      float h[6], j[3];
+      basis_hj(v, h, j);
+      float4* o = reinterpret_cast<float4*>(hj + q * 12);
+      o[0] = make_float4(h[0], h[1], h[2], h[3]);
+      o[1] = make_float4(h[4], h[5], j[0], j[1]);
+      o[2] = make_float4(j[2], 0.0f, 0.0f, 0.0f);
+    }
   }
   if (code) atomicMin(err, ((unsigned long long)q << 8) | (unsigned long long)code);
 }
 
 void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
-                     unsigned long long* err, cudaStream_t st) {
+                     unsigned long long* err, float* hj, cudaStream_t st) {
   if (n_jobs <= 0) return;
   int bs = 256;
-  k_validate<<<(unsigned)((n_jobs + bs - 1) / bs), bs, 0, st>>>(features, n_rows, jobs, n_jobs, err);
+  k_validate<<<(unsigned)((n_jobs + bs - 1) / bs), bs, 0, st>>>(features, n_rows, jobs, n_jobs, err, hj);
 }
 
 // ---------------------------------------------------------------------------
-// a2 + a3: basis and projection. Thread per (job, slice, padded cap):
+// a3: projection (the exact factorisation of P:L458). For job n, slice s, cap p:
 //   U = C[p][s] . H(F_n),  V = D[p][s] . J(F_n)   (the two dot products of P:L458)
-//   ka = K*(U - alpha),   kb = K*V               (exact power-of-two scaling)
+//   ka = K*(U - alpha),   kb = K*V               (exact power-of-two scaling,
+//                                                 flushed / clamped: cosched_internal.h)
+//   w[slot][state] = (U[s_slot] + sum_{l != slot} V[s_l]) * fl(1/P)
+// One function per quantity, shared by the projection and the gather kernels,
+// so both compute bit-identical values.
 // Padding caps (p >= n_caps) get kPadMargin (-FLT_MAX) so every candidate using them is infeasible.
-__device__ __forceinline__ float dot_u(const float* __restrict__ C, const float h[6]) {
-  float u = __fmul_rn(C[0], h[0]);
+__device__ __forceinline__ float dot_u(const float c[6], const float h[6]) {
+  float u = __fmul_rn(c[0], h[0]);
 #pragma unroll
-  for (int t = 1; t < 6; t++) u = __fmaf_rn(C[t], h[t], u);
+  for (int t = 1; t < 6; t++) u = __fmaf_rn(c[t], h[t], u);
   return u;
 }
-__device__ __forceinline__ float dot_v(const float* __restrict__ D, const float j[3]) {
-  float v = __fmul_rn(D[0], j[0]);
+__device__ __forceinline__ float dot_v(const float d[3], const float j[3]) {
+  float v = __fmul_rn(d[0], j[0]);
 #pragma unroll
-  for (int t = 1; t < 3; t++) v = __fmaf_rn(D[t], j[t], v);
+  for (int t = 1; t < 3; t++) v = __fmaf_rn(d[t], j[t], v);
   return v;
 }
-
-// Row-per-warp projection: a warp owns one row of a projection array and its
-// lanes are the caps p (coalesced 4-byte stores); every lane recomputes the
-// job's basis (3 divisions), which is cheaper than sharing it. One launch
-// writes the ka/kb rows ([slice][job]), the w rows ([slot][state][job]) and the
-// per-slot min/max of w (warp + block reduction, then one atomic per block).
-__device__ __forceinline__ void wrow_value(const float* __restrict__ F, const int32_t* __restrict__ jobs,
-                                           const SpaceParams& sp, const float* __restrict__ coef_c,
-                                           const float* __restrict__ coef_d, int64_t n, int slot, int s, int p,
-                                           float* out) {
-  const int64_t row = jobs ? (int64_t)jobs[n] : n;
-  float h[6], j[3];
-  basis_hj(F + row * 8, h, j);
-  float acc = dot_u(coef_c + ((int64_t)p * sp.n_slices + sp.slice[s][slot]) * 6, h);
-  for (int l = 0; l < sp.n_slots; l++)
-    if (l != slot) acc = __fadd_rn(acc, dot_v(coef_d + ((int64_t)p * sp.n_slices + sp.slice[s][l]) * 3, j));
-  *out = __fmul_rn(acc, sp.inv_p[p]);
+__device__ __forceinline__ void load_hj(const float* __restrict__ hj, int64_t n, float h[6], float j[3]) {
+  const float4* q = reinterpret_cast<const float4*>(hj + n * 12);
+  const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  h[0] = a.x; h[1] = a.y; h[2] = a.z; h[3] = a.w; h[4] = b.x; h[5] = b.y;
+  j[0] = b.z; j[1] = b.w; j[2] = c.x;
+}
+__device__ __forceinline__ float flush_clamp(float x) {
+  x = fminf(fmaxf(x, -kClampAbs), kClampAbs);  // no overflow in a sum of three, no NaN against the padding
+  return fabsf(x) < kFlushBelow ? 0.0f : x;    // nonzero operands are multiples of 8: margins are 0 or >= 8
 }
 
-__global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F, const int32_t* __restrict__ jobs,
-                                                     int64_t n_jobs, const SpaceParams sp,
-                                                     const float* __restrict__ coef_c,
-                                                     const float* __restrict__ coef_d,
-                                                     const unsigned long long* __restrict__ err,
-                                                     float* __restrict__ ka, float* __restrict__ kb,
-                                                     float* __restrict__ w, unsigned* wmm) {
-  __shared__ unsigned s_mm[2 * kMaxSlots];
-  if (threadIdx.x < 2 * kMaxSlots) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
+// The coefficient rows one (slot, state or slice, cap) needs, held in registers
+// by the lane that owns that column while it loops over jobs.
+struct CoefRow {
+  float c[6];                   // C[p][slice of the slot]
+  float d[kMaxSlots][3];        // D[p][slice]: [0] for a kb row; for a w row D of the other slots, ascending
+  float inv_p;
+};
+__device__ __forceinline__ void load_c(CoefRow& r, const SpaceParams& sp, const float* __restrict__ coef_c, int slice,
+                                       int p) {
+#pragma unroll
+  for (int t = 0; t < 6; t++) r.c[t] = __ldg(coef_c + ((int64_t)p * sp.n_slices + slice) * 6 + t);
+}
+__device__ __forceinline__ void load_d(float d[3], const SpaceParams& sp, const float* __restrict__ coef_d, int slice,
+                                       int p) {
+#pragma unroll
+  for (int t = 0; t < 3; t++) d[t] = __ldg(coef_d + ((int64_t)p * sp.n_slices + slice) * 3 + t);
+}
+// w row of (slot, state s) at cap p: C of the slot's slice, D of the other slots' slices
+__device__ __forceinline__ void load_w_row(CoefRow& r, const SpaceParams& sp, const float* __restrict__ coef_c,
+                                           const float* __restrict__ coef_d, int slot, int s, int p) {
+  load_c(r, sp, coef_c, sp.slice[s][slot], p);
+  int k = 0;
+  for (int l = 0; l < sp.n_slots; l++)
+    if (l != slot) load_d(r.d[k++], sp, coef_d, sp.slice[s][l], p);
+  r.inv_p = sp.inv_p[p];
+}
+__device__ __forceinline__ float ka_value(const SpaceParams& sp, const CoefRow& r, const float h[6]) {
+  return flush_clamp(__fmul_rn(__fsub_rn(dot_u(r.c, h), sp.alpha), kScale));
+}
+__device__ __forceinline__ float kb_value(const CoefRow& r, const float j[3]) {
+  return flush_clamp(__fmul_rn(dot_v(r.d[0], j), kScale));
+}
+__device__ __forceinline__ float w_value(const SpaceParams& sp, const CoefRow& r, const float h[6], const float j[3]) {
+  float acc = dot_u(r.c, h);
+  for (int k = 0; k + 1 < sp.n_slots; k++) acc = __fadd_rn(acc, dot_v(r.d[k], j));
+  return __fmul_rn(acc, r.inv_p);
+}
+
+// Both kernels below: a thread owns a job (its basis in registers, one
+// coalesced 48-byte load), loops over the columns of its row (caps or the 20
+// configs of a stage) with the columns' coefficient rows broadcast from shared
+// memory, and writes the row into a per-warp staging tile; the warp then stores
+// its 32 consecutive rows, which are contiguous in global memory, with
+// coalesced stores.
+constexpr int kProjWarps = 4;
+constexpr int kProjJobs = 32 * kProjWarps;
+
+// Grid (x: blocks of kProjJobs jobs, y: row kind): y < n_slices -> the ka and kb
+// rows of slice y; else the w row of (slot, state) = divmod(y - n_slices,
+// n_states). The per-slot min/max of w is reduced per block, then one atomic
+// per block.
+__global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restrict__ hj, int64_t n_jobs,
+                                                           const SpaceParams sp, const float* __restrict__ coef_c,
+                                                           const float* __restrict__ coef_d,
+                                                           const unsigned long long* __restrict__ err,
+                                                           float* __restrict__ ka, float* __restrict__ kb,
+                                                           float* __restrict__ w, unsigned* wmm) {
+  __shared__ CoefRow s_coef[kMaxCaps];
+  __shared__ unsigned s_mm[2];
+  extern __shared__ float s_stage[];  // [kProjWarps][32][rs + 1]
+  const int y = blockIdx.y;
+  const bool is_w = y >= sp.n_slices;
+  const int slot = is_w ? (y - sp.n_slices) / sp.n_states : 0, state = is_w ? (y - sp.n_slices) % sp.n_states : 0;
+  for (int p = threadIdx.x; p < sp.n_caps; p += blockDim.x) {
+    CoefRow r;
+    if (!is_w) {
+      load_c(r, sp, coef_c, y, p);
+      load_d(r.d[0], sp, coef_d, y, p);
+    } else {
+      load_w_row(r, sp, coef_c, coef_d, slot, state, p);
+    }
+    s_coef[p] = r;
+  }
+  if (threadIdx.x < 2) s_mm[threadIdx.x] = threadIdx.x ? 0u : 0xFFFFFFFFu;
   __syncthreads();
   if (*err != ~0ull) return;  // invalid input: leave the workspace untouched (uniform per launch)
-  const int lane = threadIdx.x & 31;
-  const unsigned npad = (unsigned)sp.n_jobs_pad;
-  const unsigned rows_k = (unsigned)sp.n_slices * npad;
-  const unsigned rows_w = (unsigned)(sp.n_slots * sp.n_states) * npad;
-  const unsigned wpb = blockDim.x >> 5;
-  unsigned lo[kMaxSlots], hi[kMaxSlots];
-#pragma unroll
-  for (int i = 0; i < kMaxSlots; i++) {
-    lo[i] = 0xFFFFFFFFu;
-    hi[i] = 0u;
-  }
-  for (unsigned r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows_k + rows_w; r += gridDim.x * wpb) {
-    for (int p = lane; p < sp.rs; p += 32) {
-      if (r < rows_k) {
-        const unsigned s = r / npad, n = r - s * npad;
-        const size_t o = (size_t)r * sp.rs + p;
-        if (p >= sp.n_caps || n >= n_jobs) {
-          ka[o] = kPadMargin;
-          kb[o] = kPadMargin;
-          continue;
-        }
-        const int64_t row = jobs ? (int64_t)jobs[n] : (int64_t)n;
-        float h[6], j[3];
-        basis_hj(F + row * 8, h, j);
-        const float u = dot_u(coef_c + ((int64_t)p * sp.n_slices + s) * 6, h);
-        const float v = dot_v(coef_d + ((int64_t)p * sp.n_slices + s) * 3, j);
-        // cosched_internal.h: flushed (margins are 0 or >= 8) and clamped to
-        // +-2^126 (no overflow in a sum of three, no NaN against the padding)
-        const float sa = fminf(fmaxf(__fmul_rn(__fsub_rn(u, sp.alpha), kScale), -kClampAbs), kClampAbs);
-        const float sb = fminf(fmaxf(__fmul_rn(v, kScale), -kClampAbs), kClampAbs);
-        ka[o] = fabsf(sa) < kFlushBelow ? 0.0f : sa;
-        kb[o] = fabsf(sb) < kFlushBelow ? 0.0f : sb;
-      } else {
-        const unsigned rw = r - rows_k;
-        const unsigned n = rw % npad, ss = rw / npad;
-        const int slot = (int)(ss / sp.n_states), s = (int)(ss % sp.n_states);
-        const size_t o = (size_t)rw * sp.rs + p;
-        if (p >= sp.n_caps || n >= n_jobs) {
-          w[o] = -1e30f;
-          continue;
-        }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rs = sp.rs, ld = rs + 1;
+  const size_t npad = (size_t)sp.n_jobs_pad;
+  const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
+  unsigned lo = 0xFFFFFFFFu, hi = 0u;
+  if (n0 < (int64_t)npad) {
+    float* stg = s_stage + warp * 32 * ld;
+    float h[6], j[3];
+    const bool job = n < n_jobs;
+    if (job) load_hj(hj, n, h, j);
+    const int passes = is_w ? 1 : 2;
+    for (int pass = 0; pass < passes; pass++) {
+      for (int p = 0; p < rs; p++) {
         float v;
-        wrow_value(F, jobs, sp, coef_c, coef_d, n, slot, s, p, &v);
-        w[o] = v;
-        const unsigned uo = ord_float_d(v);
-#pragma unroll
-        for (int i = 0; i < kMaxSlots; i++)
-          if (i == slot) {
-            lo[i] = uo < lo[i] ? uo : lo[i];
-            hi[i] = uo > hi[i] ? uo : hi[i];
+        if (p >= sp.n_caps || !job) {
+          v = is_w ? -1e30f : kPadMargin;
+        } else {
+          const CoefRow& r = s_coef[p];
+          if (is_w) {
+            v = w_value(sp, r, h, j);
+            const unsigned uo = ord_float_d(v);
+            lo = uo < lo ? uo : lo;
+            hi = uo > hi ? uo : hi;
+          } else {
+            v = pass == 0 ? ka_value(sp, r, h) : kb_value(r, j);
           }
+        }
+        stg[lane * ld + p] = v;
       }
+      __syncwarp();
+      float* dst = (is_w ? w + ((size_t)slot * sp.n_states + state) * npad * rs
+                         : (pass == 0 ? ka : kb) + (size_t)y * npad * rs) +
+                   (size_t)n0 * rs;
+      for (int i = 0; i < 32; i++)
+        for (int p = lane; p < rs; p += 32) dst[(size_t)i * rs + p] = stg[i * ld + p];
+      __syncwarp();
     }
   }
-#pragma unroll
-  for (int i = 0; i < kMaxSlots; i++) {
-    for (int off = 16; off > 0; off >>= 1) {
-      const unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo[i], off), b = __shfl_xor_sync(0xFFFFFFFFu, hi[i], off);
-      lo[i] = a < lo[i] ? a : lo[i];
-      hi[i] = b > hi[i] ? b : hi[i];
-    }
-    if (lane == 0 && i < sp.n_slots) {
-      atomicMin(&s_mm[2 * i], lo[i]);
-      atomicMax(&s_mm[2 * i + 1], hi[i]);
-    }
+  if (!is_w) return;
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo, off), b = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (lane == 0) {
+    atomicMin(&s_mm[0], lo);
+    atomicMax(&s_mm[1], hi);
   }
   __syncthreads();
-  if (threadIdx.x < 2 * sp.n_slots) {
-    if (threadIdx.x & 1) atomicMax(&wmm[threadIdx.x], s_mm[threadIdx.x]);
-    else atomicMin(&wmm[threadIdx.x], s_mm[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    atomicMin(&wmm[2 * slot], s_mm[0]);
+    atomicMax(&wmm[2 * slot + 1], s_mm[1]);
   }
 }
 
@@ -189,43 +242,59 @@ __global__ void __launch_bounds__(256) k_project_all(const float* __restrict__ F
 //     objective up to one quantum per slot (< 4e-7 relative for the presets)
 //     and carries the config's offset in its stage in the low 5 bits.
 // Rows are [role][stage][job][kStageRS]; padding (configs >= n_cfg, jobs >=
-// n_jobs) gets A = B = kPadMargin (infeasible) and W = 0. A warp owns one row
-// (lanes = the 20 configs of the stage) and reads the row-major ka/kb/w rows
-// written by k_project_all.
-__global__ void __launch_bounds__(256) k_gather_fast(const float* __restrict__ ka, const float* __restrict__ kb,
-                                                     const float* __restrict__ w, const SpaceParams sp,
-                                                     int64_t n_jobs, const unsigned long long* __restrict__ err,
-                                                     const unsigned* __restrict__ wmm, float* __restrict__ fast) {
-  __shared__ float s_lo[kMaxSlots];
-  __shared__ float s_inv;
+// n_jobs) gets A = B = kPadMargin (infeasible) and W = 0. Grid (x: blocks of
+// kProjJobs jobs, y: role * n_stages + stage). Values are recomputed from hj
+// with the projection's own functions (bit-identical to ka / kb / w).
+__global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restrict__ hj,
+                                                           const float* __restrict__ coef_c,
+                                                           const float* __restrict__ coef_d, const SpaceParams sp,
+                                                           int64_t n_jobs, const unsigned long long* __restrict__ err,
+                                                           const unsigned* __restrict__ wmm, float* __restrict__ fast) {
+  constexpr int ld = kStageCfg + 1;  // odd: the column writes of a warp hit distinct banks
+  __shared__ CoefRow s_coef[kStageCfg];
+  __shared__ float s_stage[kProjWarps][32 * ld];
+  __shared__ float s_lo, s_inv;
+  const int role = blockIdx.y / sp.n_stages, stage = blockIdx.y - role * sp.n_stages;
+  const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
+  const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);              // real configs in this stage
   if (threadIdx.x == 0) {
     float span = 0.0f;
-    for (int i = 0; i < sp.n_slots; i++) {
-      const float lo = unord_float_d(wmm[2 * i]), hi = unord_float_d(wmm[2 * i + 1]);
-      s_lo[i] = lo;
-      span += hi - lo;
-    }
+    for (int i = 0; i < sp.n_slots; i++) span += unord_float_d(wmm[2 * i + 1]) - unord_float_d(wmm[2 * i]);
+    s_lo = unord_float_d(wmm[2 * slot]);
     s_inv = span > 0.0f ? (float)(33554430 - sp.n_slots) / span : 0.0f;
+  }
+  if (threadIdx.x < ncol) {
+    const int c = stage * kStageCfg + threadIdx.x, st = c / sp.n_caps, p = c - st * sp.n_caps;
+    CoefRow r;
+    if (kind == sp.n_slots) {
+      load_w_row(r, sp, coef_c, coef_d, slot, st, p);
+    } else if (kind == 0) {
+      load_c(r, sp, coef_c, sp.slice[st][slot], p);
+    } else {
+      const int l = kind - 1 + (kind - 1 >= slot ? 1 : 0);  // the kind-th other slot, ascending
+      load_d(r.d[0], sp, coef_d, sp.slice[st][l], p);
+    }
+    s_coef[threadIdx.x] = r;
   }
   __syncthreads();
   if (*err != ~0ull) return;
-  const int col = threadIdx.x & 31;
-  if (col >= kStageRS) return;
-  const unsigned npad = (unsigned)sp.n_jobs_pad;
-  const unsigned rows = (unsigned)(sp.n_roles * sp.n_stages) * npad;
-  const unsigned wpb = blockDim.x >> 5;
-  for (unsigned r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
-    const unsigned job = r % npad, rs_ = r / npad;
-    const int stage = (int)(rs_ % sp.n_stages), role = (int)(rs_ / sp.n_stages);
-    const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
-    const int c = stage * kStageCfg + col;
-    const bool pad = col >= kStageCfg || c >= sp.n_cfg || job >= n_jobs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t npad = (size_t)sp.n_jobs_pad;
+  const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
+  if (n0 >= (int64_t)npad) return;
+  const float lo = s_lo, inv = s_inv;
+  float* stg = s_stage[warp];
+  const bool job = n < n_jobs;
+  float h[6], j[3];
+  if (job) load_hj(hj, n, h, j);
+#pragma unroll 4
+  for (int col = 0; col < kStageCfg; col++) {
+    const bool pad = col >= ncol || !job;
     float v;
     if (kind == sp.n_slots) {
       unsigned bits = 0u;
       if (!pad) {
-        const int s = c / sp.n_caps, p = c - s * sp.n_caps;
-        const float qf = rintf((w_row(w, sp, slot, s, job)[p] - s_lo[slot]) * s_inv);
+        const float qf = rintf((w_value(sp, s_coef[col], h, j) - lo) * inv);
         bits = (qf > 0.0f ? (unsigned)qf : 0u) << 5;
         if (slot == 0) bits += 0x00800000u;
         if (slot == sp.n_slots - 1) bits |= (unsigned)(31 - col);
@@ -234,15 +303,17 @@ __global__ void __launch_bounds__(256) k_gather_fast(const float* __restrict__ k
     } else if (pad) {
       v = kPadMargin;
     } else {
-      const int s = c / sp.n_caps, p = c - s * sp.n_caps;
-      if (kind == 0) {
-        v = ka_row(ka, sp, sp.slice[s][slot], job)[p];
-      } else {
-        const int l = kind - 1 + (kind - 1 >= slot ? 1 : 0);  // the kind-th other slot, ascending
-        v = ka_row(kb, sp, sp.slice[s][l], job)[p];
-      }
+      v = kind == 0 ? ka_value(sp, s_coef[col], h) : kb_value(s_coef[col], j);
     }
-    fast[(size_t)r * kStageRS + col] = v;
+    stg[lane * ld + col] = v;
+  }
+  __syncwarp();
+  float* dst = fast + (((size_t)role * sp.n_stages + stage) * npad + n0) * kStageRS;
+  static_assert(kStageRS == kStageCfg, "the stage row is exactly the stage's configs");
+#pragma unroll 4
+  for (int k = 0; k < kStageCfg; k++) {
+    const int e = k * 32 + lane, i = e / kStageCfg, c = e - i * kStageCfg;
+    dst[e] = stg[i * ld + c];
   }
 }
 
@@ -250,18 +321,17 @@ __global__ void k_init_wmm(unsigned* wmm) {
   if (threadIdx.x < 2 * kMaxSlots) wmm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
 }
 
-void launch_project(const float* features, const int32_t* jobs, int64_t n_jobs, const SpaceParams& sp,
-                    const DeviceTables& tb, const unsigned long long* err, float* ka, float* kb, float* w,
-                    float* fast, unsigned* wmm, cudaStream_t st) {
+void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
+                    const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
+                    cudaStream_t st) {
   if (n_jobs <= 0) return;
   k_init_wmm<<<1, 32, 0, st>>>(wmm);
-  const int64_t rows = ((int64_t)sp.n_slices + (int64_t)sp.n_slots * sp.n_states) * sp.n_jobs_pad;
-  int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
-  k_project_all<<<(unsigned)blocks, 256, 0, st>>>(features, jobs, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w,
-                                                   wmm);
-  const int64_t frows = (int64_t)sp.n_roles * sp.n_stages * sp.n_jobs_pad;
-  blocks = std::min<int64_t>((frows + 7) / 8, 148 * 16);
-  k_gather_fast<<<(unsigned)blocks, 256, 0, st>>>(ka, kb, w, sp, n_jobs, err, wmm, fast);
+  const unsigned jb = (unsigned)((sp.n_jobs_pad + kProjJobs - 1) / kProjJobs);
+  const size_t stage_bytes = (size_t)kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 35 KB (rs <= 68)
+  k_project_all<<<dim3(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states)), kProjJobs, stage_bytes, st>>>(
+      hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+  k_gather_fast<<<dim3(jb, (unsigned)(sp.n_roles * sp.n_stages)), kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp,
+                                                                                       n_jobs, err, wmm, fast);
 }
 
 // ---------------------------------------------------------------------------
