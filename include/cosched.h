@@ -215,6 +215,70 @@ int64_t cosched_last_greedy_rounds(cosched_t h);
 /* Number of kernels the library launched since create (instrumentation for bench.py). */
 int64_t cosched_kernel_launches(cosched_t h);
 
+/* ---- Calibration of the model coefficients ------------
+ *
+ * The offline step that produces coef_c / coef_d for cosched_create: "we train
+ * the model coefficients ... by the well-known least square method",
+ * "for each combination of (S, P) independently and separately":
+ * the solo-run coefficients C first, then D from co-runs.
+ *
+ * key = cap * n_slices + slice, i.e. the row of coef_c / coef_d (reading R1).
+ *   stage C: per key, C[key] = argmin_c sum (rperf - c . H(F_app))^2 over its solo samples;
+ *   stage D: per key, with r = rperf - C[key] . H(F_subject) on its co-run samples,
+ *            D[key] = argmin_d sum (r - d . sum_partners J(F_partner))^2  (the summed
+ *            partner term of P:L458).
+ * Solved in FP64 by the normal equations (Cholesky); a key is rank deficient
+ * when a pivot is <= 1e-10 x its column's squared norm (reading R20). Samples
+ * are grouped by key with a stable sort, so results are bit-identical run to run
+ * and independent of sample order up to FP64 rounding. */
+typedef enum {
+  COSCHED_FIT_OK = 0,
+  COSCHED_FIT_NO_SAMPLES = 1,      /* the key has no samples for this stage (D of a solo-only key: D = 0) */
+  COSCHED_FIT_INSUFFICIENT = 2,    /* fewer samples than coefficients (SPEC.md InsufficientSamples) */
+  COSCHED_FIT_RANK_DEFICIENT = 3,  /* (SPEC.md RankDeficient) */
+  COSCHED_FIT_MISSING_C = 4        /* co-run samples on a key whose C did not fit (SPEC.md MissingScalabilityCoefficients) */
+} cosched_fit_status;
+
+typedef struct {
+  int32_t n_slices, n_caps;      /* key space: n_slices * n_caps keys */
+  int32_t n_partners;            /* partners per co-run sample (n_slots - 1: 1 or 2); ignored if n_corun = 0 */
+  int64_t n_apps;                /* profiled applications */
+  const float* features;         /* device [n_apps][8] counters F1..F8 (%), validated like cosched_score_all's */
+  int64_t n_solo;                /* solo samples (< 2^31) */
+  const int32_t* solo_app;       /* device [n_solo] app index */
+  const int32_t* solo_key;       /* device [n_solo] key */
+  const float* solo_rperf;       /* device [n_solo] measured RPerf (relative to the solo, full-chip, P_max run) */
+  int64_t n_corun;               /* co-run samples, one per (run, subject slot) (< 2^31) */
+  const int32_t* co_app;         /* device [n_corun] subject app */
+  const int32_t* co_partners;    /* device [n_corun][n_partners] the co-located apps */
+  const int32_t* co_key;         /* device [n_corun] key of the subject's slice and cap */
+  const float* co_rperf;         /* device [n_corun] the subject's measured RPerf */
+} cosched_fit_desc;
+
+typedef struct {
+  double* coef_c;   /* device [n_caps][n_slices][6] (0 where the key did not fit) */
+  double* coef_d;   /* device [n_caps][n_slices][3] (0 where the key did not fit or has no co-runs) */
+  int32_t* status;  /* device [n_keys][2] cosched_fit_status of stage C and stage D */
+  int64_t* count;   /* device [n_keys][2] samples per key and stage */
+  double* rms;      /* device [n_keys][2] RMS residual of the fit (NaN where it did not fit) */
+} cosched_fit_out;
+
+/* Workspace (device bytes) cosched_fit needs for this descriptor. */
+cosched_status cosched_fit_workspace_size(const cosched_fit_desc* desc, size_t* bytes);
+
+/* Fit C and D for every key on the caller's stream and synchronise it.
+ * Returns COSCHED_OK when the inputs are valid (per-key outcomes are in
+ * out->status); COSCHED_E_RANGE / COSCHED_E_DEGENERATE_PROFILE for an invalid
+ * feature row, COSCHED_E_UNKNOWN_KEY for a key / app index out of range or a
+ * non-finite rperf (then out is unspecified; cosched_fit_last_error says which
+ * row), COSCHED_E_OOM if workspace_bytes is too small, COSCHED_E_CUDA without a
+ * device. Needs no handle and no communicator (a per-node offline step). */
+cosched_status cosched_fit(const cosched_fit_desc* desc, void* workspace, size_t workspace_bytes,
+                           const cosched_fit_out* out, void* cuda_stream);
+
+/* Message of the last failed cosched_fit in this process. */
+const char* cosched_fit_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from ._lib import INFEASIBLE, OK, STATUS, Desc, Out
 
-__all__ = ["Scheduler", "CoschedError", "n_sets", "unrank", "pack_key", "unpack_key", "shard_range_for",
+__all__ = ["Scheduler", "CoschedError", "fit", "FitResult", "n_sets", "unrank", "pack_key", "unpack_key", "shard_range_for",
            "get_unique_id", "STATUS"]
 
 
@@ -223,3 +223,55 @@ class Scheduler:
                          allow_infeasible=True)
         n = nf.value
         return st, [ids[i] for i in range(n)], [cfgs[i] for i in range(n)], tot.value
+
+
+# ---- calibration (include/cosched.h cosched_fit) ----------------
+
+class FitResult:
+    """Fitted coefficient table + per-key diagnostics (device tensors unless .cpu() is called)."""
+
+    def __init__(self, coef_c, coef_d, status, count, rms):
+        self.coef_c, self.coef_d, self.status, self.count, self.rms = coef_c, coef_d, status, count, rms
+
+    def cpu(self) -> "FitResult":
+        return FitResult(*(t.cpu().numpy() for t in (self.coef_c, self.coef_d, self.status, self.count, self.rms)))
+
+
+def fit(features, n_slices: int, n_caps: int, solo_app, solo_key, solo_rperf, co_app=None, co_partners=None,
+        co_key=None, co_rperf=None, stream=None) -> FitResult:
+    """Fit C (solo runs) then D (co-run residuals) for every key = cap * n_slices + slice.
+    All inputs are cuda tensors (features float32 [n_apps][8]; *_app / *_key / co_partners int32;
+    *_rperf float32). Synchronises the stream; raises CoschedError on invalid input."""
+    import torch
+    dev = features.device
+    L = _lib.load()
+
+    def chk(t, dt):
+        assert t.is_cuda and t.dtype == dt and t.is_contiguous()
+        return t.data_ptr()
+
+    n_co = 0 if co_app is None else int(co_app.shape[0])
+    n_part = int(co_partners.shape[1]) if (co_partners is not None and co_partners.dim() == 2) else 1
+    d = _lib.FitDesc(n_slices, n_caps, n_part if n_co else 1, features.shape[0], chk(features, torch.float32),
+                     solo_app.shape[0], chk(solo_app, torch.int32), chk(solo_key, torch.int32),
+                     chk(solo_rperf, torch.float32),
+                     n_co, chk(co_app, torch.int32) if n_co else None,
+                     chk(co_partners, torch.int32) if n_co else None,
+                     chk(co_key, torch.int32) if n_co else None, chk(co_rperf, torch.float32) if n_co else None)
+    b = ctypes.c_size_t()
+    st = L.cosched_fit_workspace_size(ctypes.byref(d), ctypes.byref(b))
+    if st != OK:
+        raise CoschedError(st, "cosched_fit_workspace_size")
+    ws = torch.empty(b.value + 256, dtype=torch.uint8, device=dev)
+    wp = (ws.data_ptr() + 255) & ~255
+    nk = n_slices * n_caps
+    C = torch.empty((n_caps, n_slices, 6), dtype=torch.float64, device=dev)
+    D = torch.empty((n_caps, n_slices, 3), dtype=torch.float64, device=dev)
+    status = torch.empty((nk, 2), dtype=torch.int32, device=dev)
+    count = torch.empty((nk, 2), dtype=torch.int64, device=dev)
+    rms = torch.empty((nk, 2), dtype=torch.float64, device=dev)
+    out = _lib.FitOut(C.data_ptr(), D.data_ptr(), status.data_ptr(), count.data_ptr(), rms.data_ptr())
+    st = L.cosched_fit(ctypes.byref(d), wp, b.value, ctypes.byref(out), _stream_handle(stream))
+    if st != OK:
+        raise CoschedError(st, (L.cosched_fit_last_error() or b"").decode())
+    return FitResult(C, D, status, count, rms)

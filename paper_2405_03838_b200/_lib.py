@@ -32,6 +32,24 @@ class Out(ctypes.Structure):
                 ("first_set", ctypes.c_int64), ("n_sets", ctypes.c_int64)]
 
 
+class FitDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_slices", ctypes.c_int32), ("n_caps", ctypes.c_int32), ("n_partners", ctypes.c_int32),
+        ("n_apps", ctypes.c_int64), ("features", ctypes.c_void_p),
+        ("n_solo", ctypes.c_int64), ("solo_app", ctypes.c_void_p), ("solo_key", ctypes.c_void_p),
+        ("solo_rperf", ctypes.c_void_p),
+        ("n_corun", ctypes.c_int64), ("co_app", ctypes.c_void_p), ("co_partners", ctypes.c_void_p),
+        ("co_key", ctypes.c_void_p), ("co_rperf", ctypes.c_void_p),
+    ]
+
+
+class FitOut(ctypes.Structure):
+    _fields_ = [("coef_c", ctypes.c_void_p), ("coef_d", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("count", ctypes.c_void_p), ("rms", ctypes.c_void_p)]
+
+
+FIT_OK, FIT_NO_SAMPLES, FIT_INSUFFICIENT, FIT_RANK_DEFICIENT, FIT_MISSING_C = 0, 1, 2, 3, 4
+
 # (name, restype, argtypes) for every symbol include/cosched.h declares
 P = ctypes.c_void_p
 I32, I64, U64, F32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
@@ -59,6 +77,9 @@ SIGNATURES = [
     ("cosched_last_timings", I32, [P, P]),
     ("cosched_kernel_launches", I64, [P]),
     ("cosched_last_greedy_rounds", I64, [P]),
+    ("cosched_fit_workspace_size", I32, [ctypes.POINTER(FitDesc), P]),
+    ("cosched_fit", I32, [ctypes.POINTER(FitDesc), P, ctypes.c_size_t, ctypes.POINTER(FitOut), P]),
+    ("cosched_fit_last_error", ctypes.c_char_p, []),
 ]
 
 _lib = None

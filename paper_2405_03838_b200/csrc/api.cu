@@ -1003,4 +1003,62 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
   return COSCHED_OK;
 }
 
+// ---- calibration (calib.cu) -------------------------------------------------------
+static thread_local std::string g_fit_error;
+
+const char* cosched_fit_last_error(void) { return g_fit_error.c_str(); }
+
+cosched_status cosched_fit_workspace_size(const cosched_fit_desc* desc, size_t* bytes) {
+  if (!bytes) return COSCHED_E_ARG;
+  cosched_status st = fit_validate_desc(desc);
+  if (st != COSCHED_OK) return st;
+  *bytes = fit_workspace_bytes(desc);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_fit(const cosched_fit_desc* desc, void* workspace, size_t workspace_bytes,
+                           const cosched_fit_out* out, void* cuda_stream) {
+  g_fit_error.clear();
+  cosched_status st = fit_validate_desc(desc);
+  if (st != COSCHED_OK) {
+    g_fit_error = "invalid descriptor";
+    return st;
+  }
+  if (!out || !out->coef_c || !out->coef_d || !out->status || !out->count || !out->rms) {
+    g_fit_error = "null output";
+    return COSCHED_E_ARG;
+  }
+  if (!workspace || workspace_bytes < fit_workspace_bytes(desc)) {
+    g_fit_error = "workspace too small";
+    return COSCHED_E_OOM;
+  }
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    g_fit_error = "no usable CUDA device";
+    return COSCHED_E_CUDA;
+  }
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  unsigned long long* err_dev = nullptr;
+  if (fit_enqueue(desc, workspace, out, &err_dev, stream) < 0) {
+    g_fit_error = std::string("launch: ") + cudaGetErrorString(cudaGetLastError());
+    return COSCHED_E_CUDA;
+  }
+  unsigned long long e = 0;
+  if (cudaMemcpyAsync(&e, err_dev, 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess) {
+    g_fit_error = std::string("CUDA: ") + cudaGetErrorString(cudaGetLastError());
+    return COSCHED_E_CUDA;
+  }
+  if (e != ~0ull) {
+    const int code = (int)(e & 0xFF);
+    const unsigned long long pos = e >> 8;
+    if (pos >= (1ull << 40))
+      g_fit_error = "sample " + std::to_string(pos - (1ull << 40)) + ": key, app or partner out of range, or rperf not finite";
+    else
+      g_fit_error = "app " + std::to_string(pos) + ": invalid counters";
+    return (cosched_status)code;
+  }
+  return COSCHED_OK;
+}
+
 }  // extern "C"

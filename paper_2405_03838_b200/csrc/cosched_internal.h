@@ -111,6 +111,11 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
                                uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
                                cudaStream_t st);
 int64_t pad_jobs(int64_t n_jobs);
+// calib.cu
+cosched_status fit_validate_desc(const cosched_fit_desc* d);
+size_t fit_workspace_bytes(const cosched_fit_desc* d);
+int fit_enqueue(const cosched_fit_desc* d, void* workspace, const cosched_fit_out* out, unsigned long long** err_dev,
+                cudaStream_t st);
 
 // ---- kernel launchers (defined in kernels.cu) ------------------------------------
 void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
