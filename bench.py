@@ -202,6 +202,48 @@ def run_reference(args):
     return 0
 
 
+def calibration_metrics(pb, F, dev, args):
+    """Time cosched_fit on a training set for the bench queue:
+    every app solo on every (slice, cap) key plus --calib-coruns co-runs, measured on the
+    synthetic GPU (synth/ground_truth.py, sigma = 0.01 noise). Device time, CUDA events."""
+    import torch
+
+    import paper_2405_03838_b200 as cs
+    from synth.ground_truth import make_training_set
+
+    ts = make_training_set(F, pb, n_corun=args.calib_coruns, seed=3000, noise=0.01)
+    d = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    targs = (d(F, np.float32), pb.n_slices, pb.n_caps, d(ts.solo_app, np.int32), d(ts.solo_key, np.int32),
+             d(ts.solo_rperf, np.float32), d(ts.co_app, np.int32), d(ts.co_partners, np.int32),
+             d(ts.co_key, np.int32), d(ts.co_rperf, np.float32))
+    for _ in range(2):
+        r = cs.fit(*targs)
+    times = []
+    stream = torch.cuda.current_stream()
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = cs.fit(*targs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    st = r.status.cpu().numpy()
+    n_solo, n_co = len(ts.solo_app), len(ts.co_app)
+    npart = ts.co_partners.shape[1] if n_co else 0
+    # algorithmic bytes: each sample record once (app, key, rperf, partners) + each app's counters
+    algo = n_solo * 12 + n_co * (12 + 4 * npart) + F.shape[0] * 32
+    peaks, src = _peaks()
+    gbs = algo / (ms * 1e-3) / 1e9
+    return {"workload": f"{args.config} queue: every app solo on every (slice, cap) key + "
+                        f"{args.calib_coruns} co-runs, synthetic GPU, sigma 0.01",
+            "n_apps": int(F.shape[0]), "n_keys": int(pb.n_slices * pb.n_caps), "solo_samples": n_solo,
+            "corun_samples": n_co, "ms": ms, "samples_per_s": (n_solo + n_co) / (ms * 1e-3),
+            "keys_fitted": [int((st[:, 0] == 0).sum()), int((st[:, 1] == 0).sum())],
+            "algorithmic_bytes": algo, "achieved_gbs": gbs, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+            "hbm_frac": gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None, "peak_source": src}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -345,6 +387,8 @@ def run_ours(args):
             "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k, "allocation_rounds": alloc_rounds,
             "clocks": clocks,
         }
+        if args.calib_coruns > 0:
+            line["calibration"] = calibration_metrics(pb, F, dev, args)
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_oracle_rate(pb, F, pb.n_slots, budget_s=args.ref_budget)
         print(json.dumps(line), flush=True)
@@ -363,6 +407,8 @@ def main():
     ap.add_argument("--variant", type=int, default=None, help="pair scorer: 1 fast (default), 0 generic")
     ap.add_argument("--alloc-k", type=int, default=5000)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--calib-coruns", type=int, default=1000000,
+                    help="co-runs of the calibration timing (0: skip the calibration measurement)")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
     args = ap.parse_args()
     if args.warmup < 3:
