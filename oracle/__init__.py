@@ -80,6 +80,11 @@ def lib():
         L.orc_greedy_allocation.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                             ctypes.c_void_p]
         L.orc_greedy_allocation.restype = ctypes.c_int64
+        L.orc_hill_climb.argtypes = [P(_Problem), ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_hill_range.argtypes = [P(_Problem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p]
     return _lib
 
 
@@ -148,6 +153,32 @@ class Oracle:
         obj = np.zeros(1)
         lib().orc_best_config_members(ctypes.byref(self.st), arr, _ptr(cfg), _ptr(obj))
         return int(cfg[0]), float(obj[0])
+
+    def hill_climb(self, rows, start_state: int, start_cap: int) -> Tuple[int, float, int]:
+        """(cfg, obj, evals) of the hill climb (reading R22) for one set of job rows."""
+        arr, keep = self._members(rows)
+        cfg = np.zeros(1, dtype=np.int32)
+        obj = np.zeros(1)
+        ev = np.zeros(1, dtype=np.int64)
+        lib().orc_hill_climb(ctypes.byref(self.st), arr, start_state, start_cap, _ptr(cfg), _ptr(obj), _ptr(ev))
+        return int(cfg[0]), float(obj[0]), int(ev[0])
+
+    def hill_range(self, F, start_state: int, start_cap: int, jobs=None, first: int = 0,
+                   count: Optional[int] = None):
+        """(cfg, obj, evals) arrays of the hill climb for every set of the range."""
+        F = np.ascontiguousarray(F, dtype=np.float32)
+        J = None if jobs is None else np.ascontiguousarray(jobs, dtype=np.int32)
+        n_jobs = F.shape[0] if J is None else J.shape[0]
+        if count is None:
+            count = n_sets(n_jobs, self.n_slots) - first
+        cfg = np.zeros(max(count, 1), dtype=np.int32)
+        obj = np.zeros(max(count, 1))
+        ev = np.zeros(max(count, 1), dtype=np.int64)
+        st = lib().orc_hill_range(ctypes.byref(self.st), _ptr(F), _ptr(J), n_jobs, first, count, start_state,
+                                  start_cap, _ptr(cfg), _ptr(obj), _ptr(ev))
+        if st:
+            raise ValueError(f"oracle hill_range status {st}")
+        return cfg[:count], obj[:count], ev[:count]
 
     # -- queue level ----------------------------------------------------------
     def score_range(self, F, jobs=None, first: int = 0, count: Optional[int] = None):

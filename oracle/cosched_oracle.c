@@ -220,6 +220,81 @@ int orc_best_config_members(const orc_problem* pb, const float* const* members, 
   return arg < 0 ? ORC_INFEASIBLE : ORC_OK;
 }
 
+/* Hill climbing over the (state x cap) grid (the
+ * heuristic P:L664 names for large spaces, "apply some heuristics here such as
+ * the hill-climbing algorithm", and P:L796). Reading R22, after
+ * SPEC.md hill_climb (L352-360):
+ *   f(c) = objective of config c if Fairness > alpha, else -inf;
+ *   climb from (s, p): evaluate the 4 grid neighbours (s-1,p), (s,p-1),
+ *   (s,p+1), (s+1,p) that exist -- in increasing config index -- and move to
+ *   the first one with the largest f if that is strictly greater than f of the
+ *   current config; stop when none is (a local optimum);
+ *   if the climb from the start ends infeasible, climb from every other config
+ *   in canonical order and return the first climb that ends feasible;
+ *   none: cfg -1, obj -inf.
+ * evals counts every f evaluation (revisits included). */
+static double hc_f(const orc_problem* pb, const float* const* members, int s, int p) {
+  double through = 0.0, fairness = INFINITY;
+  for (int i = 0; i < pb->n_slots; i++) {
+    double r = orc_rperf(pb, members, i, s, p);
+    through += r;
+    if (r < fairness) fairness = r;
+  }
+  if (!(fairness > (double)pb->alpha)) return -INFINITY;
+  return pb->objective == 1 ? through : through / (double)pb->caps_w[p];
+}
+
+static double hc_climb(const orc_problem* pb, const float* const* members, int s, int p, int* cs, int* cp,
+                       int64_t* evals) {
+  double v = hc_f(pb, members, s, p);
+  (*evals)++;
+  for (;;) {
+    const int ns[4] = {s - 1, s, s, s + 1}, np[4] = {p, p - 1, p + 1, p};
+    int bs = -1, bp = -1;
+    double bv = v;
+    for (int k = 0; k < 4; k++) {
+      if (ns[k] < 0 || ns[k] >= pb->n_states || np[k] < 0 || np[k] >= pb->n_caps) continue;
+      double w = hc_f(pb, members, ns[k], np[k]);
+      (*evals)++;
+      if (w > bv) {
+        bv = w;
+        bs = ns[k];
+        bp = np[k];
+      }
+    }
+    if (bs < 0) break;
+    s = bs;
+    p = bp;
+    v = bv;
+  }
+  *cs = s;
+  *cp = p;
+  return v;
+}
+
+int orc_hill_climb(const orc_problem* pb, const float* const* members, int start_state, int start_cap,
+                   int32_t* cfg, double* obj, int64_t* evals) {
+  int s, p;
+  int64_t ev = 0;
+  double v = hc_climb(pb, members, start_state, start_cap, &s, &p, &ev);
+  if (v == -INFINITY) {
+    const int start = start_state * pb->n_caps + start_cap;
+    for (int c = 0; c < pb->n_states * pb->n_caps && v == -INFINITY; c++) {
+      if (c == start) continue;
+      v = hc_climb(pb, members, c / pb->n_caps, c % pb->n_caps, &s, &p, &ev);
+    }
+  }
+  if (evals) *evals = ev;
+  if (v == -INFINITY) {
+    *cfg = -1;
+    *obj = -INFINITY;
+    return ORC_INFEASIBLE;
+  }
+  *cfg = s * pb->n_caps + p;
+  *obj = v;
+  return ORC_OK;
+}
+
 /* C(n, k) for k in {1, 2, 3}: the number of unordered k-job sets. */
 int64_t orc_n_sets(int64_t n_jobs, int n_slots) {
   if (n_jobs < n_slots) return 0;
@@ -281,6 +356,30 @@ int orc_score_range(const orc_problem* pb, const float* features, const int32_t*
   for (int64_t q = 0; q < count; q++) {
     gather(features, jobs, pos, pb->n_slots, members);
     orc_best_config_members(pb, members, &cfg_out[q], &obj_out[q]);
+    colex_next(pos, pb->n_slots);
+  }
+  return ORC_OK;
+}
+
+/* Hill climbing for every set of [first, first + count) (as orc_score_range). */
+int orc_hill_range(const orc_problem* pb, const float* features, const int32_t* jobs, int64_t n_jobs,
+                   int64_t first, int64_t count, int start_state, int start_cap, int32_t* cfg_out,
+                   double* obj_out, int64_t* evals_out) {
+  int st = orc_validate_problem(pb, NULL, 0);
+  if (st) return st;
+  if (start_state < 0 || start_state >= pb->n_states || start_cap < 0 || start_cap >= pb->n_caps) return ORC_E_ARG;
+  if (count <= 0) return ORC_OK;
+  int64_t pos[3];
+  if (orc_unrank(n_jobs, pb->n_slots, first, pos)) return ORC_E_ARG;
+  const float* members[3];
+  for (int64_t q = 0; q < count; q++) {
+    for (int i = 0; i < pb->n_slots; i++) {
+      int64_t row = jobs ? (int64_t)jobs[pos[i]] : pos[i];
+      members[i] = features + row * 8;
+    }
+    int64_t ev = 0;
+    orc_hill_climb(pb, members, start_state, start_cap, &cfg_out[q], &obj_out[q], &ev);
+    if (evals_out) evals_out[q] = ev;
     colex_next(pos, pb->n_slots);
   }
   return ORC_OK;

@@ -83,6 +83,13 @@ int orc_best_config_members(const orc_problem* pb, const float* const* members, 
 
 /* Number of sets C(n_jobs, n_slots), by the plain product formula. */
 int64_t orc_n_sets(int64_t n_jobs, int n_slots);
+/* Hill climbing over the (state x cap) grid from (start_state, start_cap) with the
+ * infeasible-start fallback (reading R22). */
+int orc_hill_climb(const orc_problem* pb, const float* const* members, int start_state, int start_cap,
+                   int32_t* cfg, double* obj, int64_t* evals);
+int orc_hill_range(const orc_problem* pb, const float* features, const int32_t* jobs, int64_t n_jobs,
+                   int64_t first, int64_t count, int start_state, int start_cap, int32_t* cfg_out,
+                   double* obj_out, int64_t* evals_out);
 
 /* Set id -> job positions (ascending) in colex order, by plain enumeration search. */
 int orc_unrank(int64_t n_jobs, int n_slots, int64_t set_id, int64_t* pos);
