@@ -204,6 +204,24 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
  * against). Env COSCHED_PAIR_KERNEL=generic selects 0 at create. */
 cosched_status cosched_set_variant(cosched_t h, int variant);
 
+/* Search mode of cosched_score_all (and of best_set / best_config /
+ * best_allocation, which follow the scored results):
+ *   mode 0: the exhaustive search over every (state, cap) -- default;
+ *   mode 1: hill climbing over the (state x cap) grid from (start_state,
+ *           start_cap), the heuristic P:L664 / L796 suggests for large spaces
+ *           (reading R22: steepest ascent over the 4
+ *           grid neighbours in config order, strict improvement, local optimum;
+ *           an infeasible climb restarts from every other config in canonical
+ *           order). Its objective never exceeds the exhaustive one.
+ * COSCHED_E_ARG for another mode or a start outside the grid. Marks previous
+ * results stale (call cosched_score_all again). */
+cosched_status cosched_set_search(cosched_t h, int mode, int32_t start_state, int32_t start_cap);
+
+/* Candidates (set, config) the last cosched_score_all evaluated on this rank:
+ * n_sets x n_configs for the exhaustive search, the counted evaluations of
+ * the climbs (revisits included) for hill climbing. Synchronises. */
+cosched_status cosched_last_search_evals(cosched_t h, int64_t* evals);
+
 /* Device time (ms, CUDA events on the caller's stream) of the last
  * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */

@@ -138,6 +138,15 @@ class Scheduler:
     def set_variant(self, variant: int):
         self._check(self._L.cosched_set_variant(self._h, variant))
 
+    def set_search(self, mode: int, start_state: int = 0, start_cap: int = 0):
+        """0: exhaustive search (default); 1: hill climbing from (start_state, start_cap)."""
+        self._check(self._L.cosched_set_search(self._h, mode, start_state, start_cap))
+
+    def last_search_evals(self) -> int:
+        v = ctypes.c_int64()
+        self._check(self._L.cosched_last_search_evals(self._h, ctypes.byref(v)))
+        return v.value
+
     def last_timings(self):
         """(prep_ms, score_ms, total_ms) of the last score_all, from CUDA events on its stream."""
         ms = (ctypes.c_float * 3)()

@@ -73,6 +73,8 @@ SIGNATURES = [
     ("cosched_best_config", I32, [P, I64, P, P, P, P, P]),
     ("cosched_best_allocation", I32, [P, I32, P, P, P, P]),
     ("cosched_set_variant", I32, [P, ctypes.c_int]),
+    ("cosched_set_search", I32, [P, ctypes.c_int, I32, I32]),
+    ("cosched_last_search_evals", I32, [P, P]),
     ("cosched_set_shard_view", I32, [P, ctypes.c_int, ctypes.c_int]),
     ("cosched_last_timings", I32, [P, P]),
     ("cosched_kernel_launches", I64, [P]),

@@ -297,6 +297,8 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
   sp.np = (d->n_caps + 3) & ~3;
   sp.rs = ((sp.np >> 2) & 1) ? sp.np : sp.np + 4;
   sp.n_jobs_pad = 0;
+  sp.search_mode = 0;  // exhaustive
+  sp.hc_state = sp.hc_cap = 0;
 
   sp.n_cfg = d->n_states * d->n_caps;
   sp.n_stages = (sp.n_cfg + kStageCfg - 1) / kStageCfg;
@@ -364,6 +366,33 @@ int64_t cosched_last_greedy_rounds(cosched_t h) { return h ? h->greedy_rounds : 
 cosched_status cosched_set_variant(cosched_t h, int variant) {
   if (!h || variant < 0 || variant > 1) return COSCHED_E_ARG;
   h->variant = variant;
+  return COSCHED_OK;
+}
+
+cosched_status cosched_set_search(cosched_t h, int mode, int32_t start_state, int32_t start_cap) {
+  if (!h) return COSCHED_E_ARG;
+  if (mode != 0 && mode != 1) return fail(h, COSCHED_E_ARG, "search mode must be 0 (exhaustive) or 1 (hill climb)");
+  if (mode == 1 && (start_state < 0 || start_state >= h->sp.n_states || start_cap < 0 || start_cap >= h->sp.n_caps))
+    return fail(h, COSCHED_E_ARG, "hill-climb start outside the (state, cap) grid");
+  h->sp.search_mode = mode;
+  h->sp.hc_state = mode ? start_state : 0;
+  h->sp.hc_cap = mode ? start_cap : 0;
+  h->scored = false;  // results of the other mode are stale
+  return COSCHED_OK;
+}
+
+cosched_status cosched_last_search_evals(cosched_t h, int64_t* evals) {
+  if (!h || !evals) return COSCHED_E_ARG;
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "no cosched_score_all yet");
+  if (h->sp.search_mode == 0) {
+    *evals = h->n_sets * (int64_t)h->sp.n_cfg;
+    return COSCHED_OK;
+  }
+  unsigned long long v = 0;
+  if (cudaMemcpyAsync(&v, h->ws.counters + 7, 8, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+      cudaStreamSynchronize(h->stream) != cudaSuccess)
+    return cuda_fail(h, cudaGetLastError(), "last_search_evals");
+  *evals = (int64_t)v;
   return COSCHED_OK;
 }
 
@@ -556,7 +585,14 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     h->launches += 4;
   }
   cudaEventRecord(h->ev[1], st);
-  h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key, ws.err, h->variant, st);
+  if (h->sp.search_mode == 1) {
+    launch_fill_u64((unsigned long long*)(ws.counters + 7), 0ull, 1, st);
+    h->launches += 1 + launch_score_hill(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key,
+                                         (unsigned long long*)(ws.counters + 7), ws.err, st);
+  } else {
+    h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
+                                ws.err, h->variant, st);
+  }
   cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
@@ -813,8 +849,13 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
     // score every set of the (tiny) queue locally: no collective needed
     int64_t all = cosched::n_sets(N, ns);
     launch_fill_u64(h->d_small_key, 0ull, 2, h->stream);
-    h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, h->ws.fast, 0, all, h->d_small_obj, h->d_small_cfg,
-                                    h->d_small_key, h->ws.err, h->variant, h->stream);
+    if (h->sp.search_mode == 1)
+      h->launches += 1 + launch_score_hill(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, 0, all, h->d_small_obj,
+                                           h->d_small_cfg, h->d_small_key, (unsigned long long*)(h->ws.counters + 6),
+                                           h->ws.err, h->stream);
+    else
+      h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, h->ws.fast, 0, all, h->d_small_obj,
+                                      h->d_small_cfg, h->d_small_key, h->ws.err, h->variant, h->stream);
     int64_t nm = n_partitions(ns, N);
     launch_exact_alloc(ns, N, h->d_small_obj, nm, h->d_small_key + 1, h->stream);
     launch_exact_unrank(ns, N, h->d_small_key + 1, h->d_small_ids, h->stream);

@@ -51,6 +51,8 @@ struct SpaceParams {
   int32_t n_roles;            // n_slots * (n_slots + 1) operand roles of the gathered layout
   int32_t n_cfg;              // n_states * n_caps
   float alpha;
+  int32_t search_mode;        // 0 exhaustive, 1 hill climbing from (hc_state, hc_cap) (R22)
+  int32_t hc_state, hc_cap;
   float inv_p[kMaxCaps];      // per cap: fl(1/P) (Problem 2) or 1 (Problem 1)
   int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
 };
@@ -123,6 +125,10 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
                     cudaStream_t st);
+// Hill climbing for sets [first, first+count) (search_mode 1); adds the f evaluations to *evals.
+int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
+                      int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                      unsigned long long* evals, const unsigned long long* err, cudaStream_t st);
 // Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
 // maxes the packed key into *best_key. Returns the number of kernels launched.
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,

@@ -60,6 +60,73 @@ __device__ __forceinline__ void eval_cfg(const SP& sp, const float* __restrict__
   }
 }
 
+// ---- hill climbing over the (state x cap) grid (NEXT #2; R22) ----
+// f(c) = objective of config c if every margin is positive (Fairness > alpha), else -inf,
+// in the canonical FP32 order of eval_cfg.
+template <int NS, typename SP>
+__device__ __forceinline__ float hc_value(const SP& sp, const float* __restrict__ ka, const float* __restrict__ kb,
+                                          const float* __restrict__ w, const int64_t* j, int s, int p) {
+  float r[NS], o;
+  eval_cfg<NS>(sp, ka, kb, w, j, s, p, r, &o);
+  bool feas = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) feas = feas && (r[i] > 0.0f);
+  return feas ? o : -INFINITY;
+}
+
+// Steepest ascent from (*s, *p): the existing 4-neighbours in increasing config
+// index, move to the first largest if strictly better; stop at a local optimum.
+template <int NS, typename SP>
+__device__ float hc_climb(const SP& sp, const float* __restrict__ ka, const float* __restrict__ kb,
+                          const float* __restrict__ w, const int64_t* j, int* s_io, int* p_io, int* evals) {
+  int s = *s_io, p = *p_io;
+  float v = hc_value<NS>(sp, ka, kb, w, j, s, p);
+  (*evals)++;
+  for (;;) {
+    int bs = -1, bp = -1;
+    float bv = v;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int ns = s + (k == 0 ? -1 : (k == 3 ? 1 : 0)), np = p + (k == 1 ? -1 : (k == 2 ? 1 : 0));
+      if (ns < 0 || ns >= sp.n_states || np < 0 || np >= sp.n_caps) continue;
+      const float u = hc_value<NS>(sp, ka, kb, w, j, ns, np);
+      (*evals)++;
+      if (u > bv) {
+        bv = u;
+        bs = ns;
+        bp = np;
+      }
+    }
+    if (bs < 0) break;
+    s = bs;
+    p = bp;
+    v = bv;
+  }
+  *s_io = s;
+  *p_io = p;
+  return v;
+}
+
+// The search of R22: climb from the start; if that ends infeasible, climb from every
+// other config in canonical order until one ends feasible. Returns cfg (-1: none).
+template <int NS, typename SP>
+__device__ int hill_search(const SP& sp, const float* __restrict__ ka, const float* __restrict__ kb,
+                           const float* __restrict__ w, const int64_t* j, int s0, int p0, float* obj, int* evals) {
+  int s = s0, p = p0;
+  float v = hc_climb<NS>(sp, ka, kb, w, j, &s, &p, evals);
+  if (v == -INFINITY) {
+    const int start = s0 * sp.n_caps + p0;
+    for (int c = 0; c < sp.n_cfg && v == -INFINITY; c++) {
+      if (c == start) continue;
+      s = c / sp.n_caps;
+      p = c - s * sp.n_caps;
+      v = hc_climb<NS>(sp, ka, kb, w, j, &s, &p, evals);
+    }
+  }
+  *obj = v;
+  return v == -INFINITY ? -1 : s * sp.n_caps + p;
+}
+
 // order-preserving float -> u32 (larger float <=> larger u32; -0 < +0)
 __device__ __forceinline__ uint32_t ord_float_d(float f) {
   uint32_t b = __float_as_uint(f);

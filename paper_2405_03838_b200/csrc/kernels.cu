@@ -378,6 +378,52 @@ __global__ void __launch_bounds__(256) k_score_generic(const SpaceParams sp, int
   block_max_key(key, best_key);
 }
 
+// NEXT #2: hill climbing per set (R22), one thread per set; evaluations
+// counted per block (one atomic per block).
+template <int NS>
+__global__ void __launch_bounds__(256) k_score_hill(const SpaceParams sp, const float* __restrict__ ka,
+                                                    const float* __restrict__ kb, const float* __restrict__ w,
+                                                    int64_t first, int64_t count, float* __restrict__ out_obj,
+                                                    int32_t* __restrict__ out_cfg,
+                                                    unsigned long long* __restrict__ best_key,
+                                                    unsigned long long* __restrict__ evals,
+                                                    const unsigned long long* __restrict__ err) {
+  __shared__ unsigned long long s_ev;
+  if (threadIdx.x == 0) s_ev = 0;
+  __syncthreads();
+  if (*err != ~0ull) return;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long key = 0;
+  if (k < count) {
+    const int64_t sid = first + k;
+    int64_t j[3];
+    unrank_set<NS>(sid, j);
+    float o;
+    int ev = 0;
+    const int c = hill_search<NS>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
+    if (out_obj) out_obj[k] = c >= 0 ? o : -INFINITY;
+    if (out_cfg) out_cfg[k] = c;
+    key = c >= 0 ? pack_key(o, sid) : 0ull;
+    atomicAdd(&s_ev, (unsigned long long)ev);
+  }
+  block_max_key(key, best_key);
+  if (threadIdx.x == 0) atomicAdd(evals, s_ev);
+}
+
+int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
+                      int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                      unsigned long long* evals, const unsigned long long* err, cudaStream_t st) {
+  if (count <= 0) return 0;
+  const unsigned grid = (unsigned)((count + 255) / 256);
+  if (sp.n_slots == 1)
+    k_score_hill<1><<<grid, 256, 0, st>>>(sp, ka, kb, w, first, count, obj, cfg, best_key, evals, err);
+  else if (sp.n_slots == 2)
+    k_score_hill<2><<<grid, 256, 0, st>>>(sp, ka, kb, w, first, count, obj, cfg, best_key, evals, err);
+  else
+    k_score_hill<3><<<grid, 256, 0, st>>>(sp, ka, kb, w, first, count, obj, cfg, best_key, evals, err);
+  return 1;
+}
+
 int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                             const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
                             const unsigned long long* err, cudaStream_t st);
@@ -421,6 +467,16 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
   else if (sp.n_slots == 2) unrank_set<2>(set_id, j);
   else unrank_set<3>(set_id, j);
   unsigned long long key = 0;
+  if (sp.search_mode == 1) {  // the hill climb's choice (R22), not the exhaustive argmax
+    if (threadIdx.x == 0) {
+      float o;
+      int ev = 0, c;
+      if (sp.n_slots == 1) c = hill_search<1>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
+      else if (sp.n_slots == 2) c = hill_search<2>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
+      else c = hill_search<3>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
+      key = c >= 0 ? (((unsigned long long)ord_float_d(o) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
+    }
+  } else
   for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
     int s = c / sp.n_caps, p = c % sp.n_caps;
     float r[3], u;

@@ -1,0 +1,146 @@
+"""GPU hill climbing (cosched_set_search mode 1, NEXT #2) vs the oracle's climb
+(orc_hill_climb, reading R22) on seeded synthetic queues.
+
+Bar: the chosen config equals the oracle's on every set whose climb takes no
+near-tie decision; where FP32 and FP64 take a different branch at a near-tie
+(objectives within 1e-5 relative), the GPU's result must still be a valid
+outcome of the algorithm under the oracle's values: feasible, a local optimum
+of the oracle landscape up to the tolerance, and never better than the
+exhaustive optimum. Evaluation counts match wherever the configs match.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import Oracle  # noqa: E402
+from synth import bench_config, make_features, make_problem  # noqa: E402
+from parity import TAU_F, TAU_OBJ  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_03838_b200 as cs
+    return cs
+
+
+def _hill(cs, pb, F, start, jobs=None):
+    s = cs.Scheduler(pb)
+    s.set_search(1, *start)
+    Fd = torch.from_numpy(np.ascontiguousarray(F)).cuda()
+    Jd = None if jobs is None else torch.from_numpy(np.ascontiguousarray(jobs, dtype=np.int32)).cuda()
+    obj, cfg = s.score_all(Fd, Jd)
+    torch.cuda.synchronize()
+    return s, obj.cpu().numpy(), cfg.cpu().numpy()
+
+
+def _valid_local_optimum(o, pb, rows, c, obj_g):
+    """c is a feasible (loose) local optimum of the oracle's landscape up to TAU_OBJ, its
+    objective agrees with the GPU's, and it does not beat the exhaustive optimum."""
+    objs, fair, _, feas, _ = o.eval_set(rows)
+    alpha = float(np.float32(pb.alpha))
+    loose = fair > alpha - TAU_F
+    strict = fair > alpha + TAU_F
+    if c < 0:  # the fallback climbs from every config: -1 means no config is feasible
+        return not strict.any()
+    if not loose[c] or abs(obj_g - objs[c]) > TAU_OBJ * abs(objs[c]):
+        return False
+    ns, nc = pb.n_states, pb.n_caps
+    s, p = divmod(c, nc)
+    for ds, dp in ((-1, 0), (1, 0), (0, -1), (0, 1)):
+        t, q = s + ds, p + dp
+        if 0 <= t < ns and 0 <= q < nc and strict[t * nc + q] and objs[t * nc + q] > objs[c] * (1 + TAU_OBJ):
+            return False
+    best = objs[strict].max() if strict.any() else -math.inf
+    return objs[c] <= best * (1 + TAU_OBJ) or not strict.any()
+
+
+def _parity(cs, pb, F, start, jobs=None, min_exact=0.999):
+    s, obj_g, cfg_g = _hill(cs, pb, F, start, jobs)
+    o = Oracle(pb)
+    cfg_o, obj_o, ev_o = o.hill_range(F, *start, jobs=jobs)
+    assert len(cfg_o) == len(cfg_g)
+    same = cfg_g == cfg_o
+    assert same.mean() >= min_exact, same.mean()
+    m = same & (cfg_o >= 0)
+    assert np.all(np.abs(obj_g[m] - obj_o[m]) <= TAU_OBJ * np.abs(obj_o[m]))
+    n = F.shape[0] if jobs is None else len(jobs)
+    for sid in np.nonzero(~same)[0][:200]:
+        rows = [F[p] if jobs is None else F[jobs[p]] for p in oracle.unrank(n, pb.n_slots, int(sid))]
+        assert _valid_local_optimum(o, pb, rows, int(cfg_g[sid]), float(obj_g[sid])), sid
+    # the ABI reports the total evaluation count: it equals the oracle's when every path matched
+    ev = s.last_search_evals()
+    if same.all():
+        assert ev == int(ev_o.sum())
+    return s, obj_g, cfg_g, cfg_o, obj_o
+
+
+@pytest.mark.parametrize("start", [(0, 0), (6, 9), (13, 5)])
+def test_pairs_c3_subset(cs, start):
+    pb, F = bench_config("C3")
+    _parity(cs, pb, F[:300], start)
+
+
+@pytest.mark.parametrize("n", [2, 3, 65, 130])
+def test_ragged_and_tiny(cs, n):
+    pb = make_problem("b200", "c21", coef_seed=80 + n, alpha=0.5)
+    F, _ = make_features(n, seed=80 + n)
+    _parity(cs, pb, F, (0, pb.n_caps - 1))
+
+
+def test_triples_and_solo(cs):
+    pb = make_problem("b200_3way", "c10", coef_seed=90, alpha=0.2)
+    F, _ = make_features(30, seed=90)
+    _parity(cs, pb, F, (20, 3))
+    pb1 = make_problem("solo", "c10", coef_seed=91, objective=1, alpha=0.0)
+    F1, _ = make_features(100, seed=91)
+    _parity(cs, pb1, F1, (0, 0))
+
+
+def test_hill_never_beats_exhaustive_on_gpu(cs):
+    """Same FP32 landscape on both sides: every hill objective <= the exhaustive one, exactly."""
+    pb, F = bench_config("C3")
+    F = F[:400]
+    s, obj_h, cfg_h = _hill(cs, pb, F, (0, 0))
+    s2 = cs.Scheduler(pb)
+    obj_e, cfg_e = s2.score_all(torch.from_numpy(F).cuda())
+    torch.cuda.synchronize()
+    obj_e, cfg_e = obj_e.cpu().numpy(), cfg_e.cpu().numpy()
+    assert np.all(obj_h <= obj_e)
+    assert np.all((cfg_h >= 0) == (cfg_e >= 0))  # the fallback scan finds a feasible config iff one exists
+
+
+def test_infeasible_best_set_and_config_follow_the_climb(cs):
+    pb = make_problem("b200", "c10", coef_seed=92, alpha=10.0)
+    F, _ = make_features(20, seed=92)
+    s, obj_g, cfg_g = _hill(cs, pb, F, (0, 0))
+    assert (cfg_g == -1).all() and s.best_set()[0] == 2
+    pb = make_problem("b200", "c10", coef_seed=93, alpha=0.3)
+    F, _ = make_features(40, seed=93)
+    s, obj_g, cfg_g = _hill(cs, pb, F, (2, 2))
+    st, sid, cfg, ob = s.best_set()
+    assert st == 0 and cfg == cfg_g[sid] and ob == obj_g[sid] and ob == obj_g.max()
+    d = s.best_config(sid)
+    assert d["cfg"] == cfg_g[sid] and d["obj"] == obj_g[sid]
+    with pytest.raises(cs.CoschedError):
+        s.set_search(1, pb.n_states, 0)
+    with pytest.raises(cs.CoschedError):
+        s.set_search(2, 0, 0)
+
+
+def test_exact_allocation_on_hill_objectives(cs):
+    """The allocation uses the per-set objectives of the active search mode."""
+    pb, F = bench_config("C2")
+    s, obj_g, cfg_g = _hill(cs, pb, F, (0, 0))
+    st, ids, cfgs, tot = s.best_allocation(4)
+    cfg_o, obj_o, _ = Oracle(pb).hill_range(F, 0, 0)
+    ost, rank, oids, otot, nmatch = oracle.exact_allocation(8, 2, obj_o)
+    assert st == ost == 0 and nmatch == 105
+    assert ids == oids or sum(obj_o[i] for i in ids) >= otot * (1 - TAU_OBJ)
+    assert cfgs == [int(cfg_g[i]) for i in ids]
