@@ -244,6 +244,35 @@ def calibration_metrics(pb, F, dev, args):
             "hbm_frac": gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None, "peak_source": src}
 
 
+def hill_metrics(sched, Fd, pb, stream, args):
+    """Hill climbing (cosched_set_search mode 1, NEXT #2) over the same queue: device time,
+    evaluations, and decision quality against the exhaustive search just timed."""
+    import torch
+    obj_e, cfg_e = sched.score_all(Fd, None, with_out=True, stream=stream)
+    obj_e, cfg_e = obj_e.clone(), cfg_e.clone()
+    start = (0, pb.n_caps - 1)
+    sched.set_search(1, *start)
+    times = []
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        obj_h, cfg_h = sched.score_all(Fd, None, with_out=True, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    evals = sched.last_search_evals()
+    feas = (cfg_e >= 0) & (cfg_h >= 0)
+    ratio = (obj_h[feas].double() / obj_e[feas].double())
+    out = {"start": {"state": start[0], "cap": start[1]}, "ms": min(times), "sets": int(cfg_e.numel()),
+           "evals": int(evals), "evals_per_set": evals / max(cfg_e.numel(), 1),
+           "evals_per_s": evals / (min(times) * 1e-3),
+           "same_config_as_exhaustive": float((cfg_h == cfg_e).double().mean().item()),
+           "objective_ratio_mean": float(ratio.mean().item()) if ratio.numel() else None,
+           "objective_ratio_geomean": float(torch.exp(torch.log(ratio).mean()).item()) if ratio.numel() else None}
+    sched.set_search(0)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -387,6 +416,8 @@ def run_ours(args):
             "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k, "allocation_rounds": alloc_rounds,
             "clocks": clocks,
         }
+        if args.hill:
+            line["hill_climb"] = hill_metrics(sched, Fd, pb, stream, args)
         if args.calib_coruns > 0:
             line["calibration"] = calibration_metrics(pb, F, dev, args)
         if args.cpu_baseline and world == 1:
@@ -407,6 +438,7 @@ def main():
     ap.add_argument("--variant", type=int, default=None, help="pair scorer: 1 fast (default), 0 generic")
     ap.add_argument("--alloc-k", type=int, default=5000)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-hill", dest="hill", action="store_false", help="skip the hill-climbing measurement")
     ap.add_argument("--calib-coruns", type=int, default=1000000,
                     help="co-runs of the calibration timing (0: skip the calibration measurement)")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
