@@ -93,7 +93,8 @@ struct Workspace {
   size_t bytes = 0;
 };
 
-constexpr int kHistBins = 65536;
+constexpr int kHistLog2 = 14;
+constexpr int kHistBins = 1 << kHistLog2;  // greedy objective histogram (per-block copy fits shared memory)
 size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_local, int nranks, char* base,
                         Workspace* ws);
 // greedy.cu

@@ -146,24 +146,25 @@ __device__ __forceinline__ unsigned long long pack_key(float obj, int64_t sid) {
 __device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
 __device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
 
-// colex unranking: set id -> ascending queue positions
+// colex unranking: set id -> ascending queue positions. FP32 root estimates
+// (within +-2 of the answer for ids < 2^53) corrected by exact integer tests.
 template <int NS>
 __device__ __forceinline__ void unrank_set(int64_t id, int64_t* j) {
   if (NS == 1) {
     j[0] = id;
   } else if (NS == 2) {
-    int64_t b = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)id)) * 0.5);
-    while (c2(b) > id) b--;
+    int64_t b = (int64_t)((1.0f + sqrtf(1.0f + 8.0f * (float)id)) * 0.5f);
+    while (b > 1 && c2(b) > id) b--;
     while (c2(b + 1) <= id) b++;
     j[1] = b;
     j[0] = id - c2(b);
   } else {
-    int64_t c = (int64_t)cbrt(6.0 * (double)id) + 1;
-    while (c3(c) > id) c--;
+    int64_t c = (int64_t)cbrtf(6.0f * (float)id) + 1;
+    while (c > 2 && c3(c) > id) c--;
     while (c3(c + 1) <= id) c++;
     int64_t rest = id - c3(c);
-    int64_t b = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)rest)) * 0.5);
-    while (c2(b) > rest) b--;
+    int64_t b = (int64_t)((1.0f + sqrtf(1.0f + 8.0f * (float)rest)) * 0.5f);
+    while (b > 1 && c2(b) > rest) b--;
     while (c2(b + 1) <= rest) b++;
     j[2] = c;
     j[1] = b;

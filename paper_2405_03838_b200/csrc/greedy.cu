@@ -27,16 +27,30 @@
 
 namespace cosched {
 
+// Objective arrays are scanned as float4 when the caller's obj pointer is
+// 16-byte aligned (then count/4 float4s and a scalar tail), else scalar.
+__device__ __forceinline__ int64_t vec4_count(const float* p, int64_t count) {
+  return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) ? (count >> 2) : 0;
+}
 __global__ void k_obj_minmax(const float* __restrict__ obj, int64_t count, unsigned* mm /* [0] min ord, [1] max ord */) {
   unsigned lo = 0xFFFFFFFFu, hi = 0u;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
-    float o = obj[k];
+  const int64_t n4 = vec4_count(obj, count), stride = (int64_t)gridDim.x * blockDim.x;
+  const float4* o4 = reinterpret_cast<const float4*>(obj);
+  auto take = [&](float o) {
     if (o > -INFINITY) {
-      unsigned u = ord_float_d(o);
+      const unsigned u = ord_float_d(o);
       lo = u < lo ? u : lo;
       hi = u > hi ? u : hi;
     }
+  };
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4; k += stride) {
+    const float4 v = __ldcs(o4 + k);
+    take(v.x);
+    take(v.y);
+    take(v.z);
+    take(v.w);
   }
+  for (int64_t k = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += stride) take(obj[k]);
   for (int off = 16; off > 0; off >>= 1) {
     unsigned a = __shfl_xor_sync(0xFFFFFFFFu, lo, off), b = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
     lo = a < lo ? a : lo;
@@ -48,41 +62,132 @@ __global__ void k_obj_minmax(const float* __restrict__ obj, int64_t count, unsig
   }
 }
 
-__device__ __forceinline__ int bin_of(unsigned u, unsigned lo, unsigned span, int nbins) {
-  return (int)(((unsigned long long)(u - lo) * (unsigned long long)nbins) / ((unsigned long long)span + 1ull));
+// Bins: kHistBins = 2^14 equal slices of [lo, hi] in ord(obj) space, bin(u) =
+// floor((u - lo) 2^14 / (span + 1)). Its first value t(b) = lo + ceil(b (span + 1)
+// / 2^14) needs only a multiply and a shift, so a bin range is a range of u and
+// the per-element bin is a floating-point estimate corrected against t (no
+// 64-bit division on the hot path).
+__device__ __forceinline__ unsigned long long bin_start(unsigned lo, unsigned span, int b) {
+  return (unsigned long long)lo +
+         (((unsigned long long)b * ((unsigned long long)span + 1ull) + ((1ull << kHistLog2) - 1ull)) >> kHistLog2);
+}
+__device__ __forceinline__ int bin_of(unsigned u, unsigned lo, unsigned span, double scale) {
+  int b = (int)((double)(u - lo) * scale);
+  b = b < 0 ? 0 : (b > kHistBins - 1 ? kHistBins - 1 : b);
+  while (b < kHistBins - 1 && bin_start(lo, span, b + 1) <= u) b++;
+  while (b > 0 && bin_start(lo, span, b) > u) b--;
+  return b;
 }
 
-__global__ void k_obj_hist(const float* __restrict__ obj, int64_t count, const unsigned* __restrict__ mm, int nbins,
-                           unsigned* hist) {
+// Histogram privatised per block in shared memory (64 KB), merged with one
+// global atomic per nonzero bin and block.
+__global__ void __launch_bounds__(1024) k_obj_hist(const float* __restrict__ obj, int64_t count,
+                                                   const unsigned* __restrict__ mm, int nbins, unsigned* hist) {
+  extern __shared__ unsigned s_hist[];
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) s_hist[i] = 0u;
+  __syncthreads();
   const unsigned lo = mm[0], span = mm[1] - mm[0];
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
-    float o = obj[k];
-    if (o > -INFINITY) atomicAdd(&hist[bin_of(ord_float_d(o), lo, span, nbins)], 1u);
+  const double scale = (double)kHistBins / ((double)span + 1.0);
+  const int64_t n4 = vec4_count(obj, count), stride = (int64_t)gridDim.x * blockDim.x;
+  const float4* o4 = reinterpret_cast<const float4*>(obj);
+  auto take = [&](float o) {
+    if (o > -INFINITY) atomicAdd(&s_hist[bin_of(ord_float_d(o), lo, span, scale)], 1u);
+  };
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4; k += stride) {
+    const float4 v = __ldcs(o4 + k);
+    take(v.x);
+    take(v.y);
+    take(v.z);
+    take(v.w);
   }
+  for (int64_t k = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += stride) take(obj[k]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
 // keys of the sets whose bin lies in [bin_lo, bin_hi] and whose jobs are all
-// still free (sets touching a taken job can never be picked again)
+// still free (sets touching a taken job can never be picked again). Two phases
+// per warp: the cheap range test on every element compacts the in-range
+// (id, obj) pairs into a per-warp shared queue; whenever 32 are queued the
+// warp decodes them one per lane (colex unranking, taken-bit test) -- so the
+// unranking runs at full lane occupancy instead of diverging on every element.
+constexpr int kKirWarps = 8;
+constexpr int kKirQueue = 32 + 4 * 32;
 template <int NS>
-__global__ void k_keys_in_range(const float* __restrict__ obj, int64_t first, int64_t count,
-                                const unsigned* __restrict__ mm, int nbins, int bin_lo, int bin_hi,
-                                const uint32_t* __restrict__ taken_bits, unsigned long long* keys,
-                                unsigned long long* n_keys) {
+__global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* __restrict__ obj, int64_t first,
+                                                                 int64_t count, const unsigned* __restrict__ mm,
+                                                                 int nbins, int bin_lo, int bin_hi,
+                                                                 const uint32_t* __restrict__ taken_bits,
+                                                                 unsigned long long* keys,
+                                                                 unsigned long long* n_keys) {
+  __shared__ int64_t s_id[kKirWarps][kKirQueue];
+  __shared__ float s_o[kKirWarps][kKirQueue];
   const unsigned lo = mm[0], span = mm[1] - mm[0];
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
-    float o = obj[k];
-    if (!(o > -INFINITY)) continue;
-    int b = bin_of(ord_float_d(o), lo, span, nbins);
-    if (b < bin_lo || b > bin_hi) continue;
-    int64_t j[3];
-    unrank_set<NS>(first + k, j);
-    bool fr = true;
+  const unsigned long long u_lo = bin_start(lo, span, bin_lo), u_hi = bin_start(lo, span, bin_hi + 1);  // [u_lo, u_hi)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int64_t* qid = s_id[wib];
+  float* qo = s_o[wib];
+  int qn = 0;  // warp-uniform queue length
+  auto in_range = [&](float o) {
+    if (!(o > -INFINITY)) return false;
+    const unsigned long long u = ord_float_d(o);
+    return u >= u_lo && u < u_hi;
+  };
+  // decode the 32 queue entries [qn - n, qn) (n <= 32), append the free ones
+  auto drain = [&](int n) {
+    unsigned long long kk = 0ull;
+    bool ok = false;
+    if (lane < n) {
+      const int64_t sid = qid[qn - n + lane];
+      int64_t j[3];
+      unrank_set<NS>(sid, j);
+      ok = true;
 #pragma unroll
-    for (int q = 0; q < NS; q++) fr = fr && !((__ldg(taken_bits + (j[q] >> 5)) >> (j[q] & 31)) & 1u);
-    if (!fr) continue;
-    unsigned long long at = atomicAdd(n_keys, 1ull);
-    keys[at] = pack_key(o, first + k);
+      for (int q = 0; q < NS; q++) ok = ok && !((__ldg(taken_bits + (j[q] >> 5)) >> (j[q] & 31)) & 1u);
+      if (ok) kk = pack_key(qo[qn - n + lane], sid);
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(n_keys, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (ok) keys[base + __popc(m & ((1u << lane) - 1u))] = kk;
+    }
+    __syncwarp();
+    qn -= n;
+  };
+  auto push = [&](bool hit, float o, int64_t sid) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+    if (hit) {
+      const int at = qn + __popc(m & ((1u << lane) - 1u));
+      qid[at] = sid;
+      qo[at] = o;
+    }
+    qn += __popc(m);
+    __syncwarp();
+  };
+  const int64_t n4 = vec4_count(obj, count);
+  const float4* o4 = reinterpret_cast<const float4*>(obj);
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k0 = gw * 32; k0 < n4; k0 += nw * 32) {
+    const int64_t k = k0 + lane;
+    float4 v = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    if (k < n4) v = __ldcs(o4 + k);
+    push(in_range(v.x), v.x, first + 4 * k);
+    push(in_range(v.y), v.y, first + 4 * k + 1);
+    push(in_range(v.z), v.z, first + 4 * k + 2);
+    push(in_range(v.w), v.w, first + 4 * k + 3);
+    while (qn >= 32) drain(32);
   }
+  // scalar tail (< 4 elements, plus everything when obj is not 16-byte aligned)
+  for (int64_t t0 = (n4 << 2) + gw * 32; t0 < count; t0 += nw * 32) {
+    const int64_t k = t0 + lane;
+    const float o = k < count ? obj[k] : -INFINITY;
+    push(k < count && in_range(o), o, first + k);
+    while (qn >= 32) drain(32);
+  }
+  if (qn > 0) drain(qn);
 }
 
 // The sequential rule over a sorted window of 1024 candidates, resolved in
@@ -261,20 +366,25 @@ void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream
 }
 void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st) {
   if (count <= 0) return;
-  int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
-  k_obj_hist<<<(unsigned)blocks, 256, 0, st>>>(obj, count, mm, nbins, hist);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_obj_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistBins * 4);
+    attr = true;
+  }
+  int64_t blocks = std::min<int64_t>((count + 1023) / 1024, 148 * 2);
+  k_obj_hist<<<(unsigned)blocks, 1024, kHistBins * 4, st>>>(obj, count, mm, nbins, hist);
 }
 void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
                           unsigned long long* n_keys, cudaStream_t st) {
   if (count <= 0) return;
-  int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  int64_t blocks = std::min<int64_t>((count + 32 * kKirWarps * 4 - 1) / (32 * kKirWarps * 4), 148 * 8);
   if (n_slots == 2)
-    k_keys_in_range<2><<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, taken_bits,
-                                                          keys, n_keys);
+    k_keys_in_range<2><<<(unsigned)blocks, 32 * kKirWarps, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi,
+                                                                    taken_bits, keys, n_keys);
   else
-    k_keys_in_range<3><<<(unsigned)blocks, 256, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi, taken_bits,
-                                                          keys, n_keys);
+    k_keys_in_range<3><<<(unsigned)blocks, 32 * kKirWarps, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi,
+                                                                    taken_bits, keys, n_keys);
 }
 
 size_t sort_temp_bytes(int64_t n) {
