@@ -761,7 +761,8 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   CK(cudaMemsetAsync(np_dev, 0, 8, s));
   int bin_hi = kHistBins - 1;
   int64_t n_picks = 0;
-  while (bin_hi >= 0 && n_picks < k) {
+  bool endgame = false;
+  while (bin_hi >= 0 && n_picks < k && !endgame) {
     int bin_lo = bin_hi;
     int64_t acc = hist[bin_hi];
     while (bin_lo > 0 && acc + hist[bin_lo - 1] <= kBatch) acc += hist[--bin_lo];
@@ -769,11 +770,23 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       bin_hi = bin_lo - 1;
       continue;
     }
-    // 3. compact this rank's keys in the range; gather over ranks; sort; scan
+    // endgame: every set that can still be picked lies among the free jobs; when
+    // there are at most kBatch of them, take them all in one final batch
+    // (sets of earlier batches were picked or blocked, so no bin filter is needed)
+    const int64_t n_free = N - (int64_t)ns * n_picks;
+    const int64_t n_comb = cosched::n_sets(n_free, ns);
+    endgame = n_picks > 0 && n_comb <= kBatch && n_comb * 8 <= cosched::n_sets(N, ns);  // gathers << a full scan
+    // 3. compact this rank's keys in the range (or of the free jobs); gather over ranks; sort; scan
     CK(cudaMemsetAsync(nk_dev, 0, 8, s));
-    launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
-                         (unsigned long long*)ws.alive, nk_dev, s);
-    h->launches++;
+    if (endgame) {
+      launch_free_sets(ns, taken_bits, N, (int32_t*)ws.job_key, ws.counters + 5, n_comb, h->out_obj, h->first,
+                       h->n_sets, (unsigned long long*)ws.alive, nk_dev, s);
+      h->launches += 2;
+    } else {
+      launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
+                           (unsigned long long*)ws.alive, nk_dev, s);
+      h->launches++;
+    }
     int64_t nk = 0;
     CK(cudaMemcpyAsync(&nk, nk_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

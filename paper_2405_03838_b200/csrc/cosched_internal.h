@@ -103,6 +103,10 @@ void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nb
 void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
                           unsigned long long* n_keys, cudaStream_t st);
+// greedy endgame: keys of every feasible set of free jobs (free list built on the device)
+void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
+                      int64_t n_comb, const float* obj, int64_t first, int64_t count, unsigned long long* keys,
+                      unsigned long long* n_keys, cudaStream_t st);
 size_t sort_temp_bytes(int64_t n);
 size_t select_temp_bytes(int64_t n);
 cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const unsigned long long* in,

@@ -190,6 +190,82 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   if (qn > 0) drain(qn);
 }
 
+// Endgame of the greedy: once few jobs are free, the sets that can still be
+// picked are exactly the sets of free jobs. Enumerate them directly (colex
+// over the ascending free-job list) instead of scanning every set's objective
+// again: C(n_free, n_slots) gathers instead of n_sets reads.
+__global__ void k_free_list(const uint32_t* __restrict__ taken_bits, int64_t n_jobs, int32_t* __restrict__ free_list,
+                            int64_t* __restrict__ n_free) {
+  // one block: ordered compaction by warp ballots
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_cnt[32];
+  for (int64_t b0 = 0; b0 < n_jobs; b0 += blockDim.x) {
+    const int64_t j = b0 + threadIdx.x;
+    const bool fr = j < n_jobs && !((taken_bits[j >> 5] >> (j & 31)) & 1u);
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, fr);
+    if (lane == 0) s_cnt[w] = __popc(m);
+    __syncthreads();
+    int off = s_base;
+    for (int q = 0; q < w; q++) off += s_cnt[q];
+    if (fr) free_list[off + __popc(m & ((1u << lane) - 1u))] = (int32_t)j;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < nw; q++) s_base += s_cnt[q];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_free = s_base;
+}
+
+template <int NS>
+__global__ void k_free_sets(const int32_t* __restrict__ free_list, int64_t n_comb, const float* __restrict__ obj,
+                            int64_t first, int64_t count, unsigned long long* keys, unsigned long long* n_keys) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; r0 < n_comb; r0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = r0 + lane;
+    bool ok = false;
+    unsigned long long kk = 0ull;
+    if (r < n_comb) {
+      int64_t q[3];
+      unrank_set<NS>(r, q);  // ascending positions in the free list
+      int64_t sid = 0;
+#pragma unroll
+      for (int i = 0; i < NS; i++) {
+        const int64_t jv = free_list[q[i]];
+        sid += (i == 0) ? jv : (i == 1 ? c2(jv) : c3(jv));  // colex rank of the ascending job tuple
+      }
+      if (sid >= first && sid < first + count) {
+        const float o = obj[sid - first];
+        if (o > -INFINITY) {
+          ok = true;
+          kk = pack_key(o, sid);
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(n_keys, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (ok) keys[base + __popc(m & ((1u << lane) - 1u))] = kk;
+    }
+  }
+}
+
+void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
+                      int64_t n_comb, const float* obj, int64_t first, int64_t count, unsigned long long* keys,
+                      unsigned long long* n_keys, cudaStream_t st) {
+  k_free_list<<<1, 1024, 0, st>>>(taken_bits, n_jobs, free_list, n_free_dev);
+  if (n_comb <= 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n_comb + 255) / 256, 148 * 8);
+  if (n_slots == 2)
+    k_free_sets<2><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys);
+  else
+    k_free_sets<3><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys);
+}
+
 // The sequential rule over a sorted window of 1024 candidates, resolved in
 // parallel: an undecided candidate whose jobs are all still free and that is
 // the lowest-index undecided candidate on every one of its jobs cannot be
