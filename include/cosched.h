@@ -121,7 +121,9 @@ const char* cosched_last_create_error(void);
 cosched_status cosched_get_unique_id(void* uid_out);
 
 /* COLLECTIVE: create the communicator from rank 0's id (host, 128 bytes).
- * nranks == 1 (uid may be NULL) resets to single-rank mode. */
+ * nranks == 1 with uid == NULL resets to single-rank mode without NCCL;
+ * nranks == 1 with an id builds a one-rank communicator (every collective of
+ * the library then runs through NCCL, as on a multi-GPU node). */
 cosched_status cosched_set_comm(cosched_t h, const void* nccl_unique_id, int rank, int nranks);
 
 /* Shard view without a communicator: score as rank `rank` of `nranks` on this

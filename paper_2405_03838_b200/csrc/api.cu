@@ -163,12 +163,13 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.alive2 = (int64_t*)take((size_t)n_sets_local * 8 + 8);
   w.hist = (unsigned*)take((size_t)kHistBins * 4);
   w.mm = (unsigned*)take(16);
-  const int64_t cap = nranks > 1 ? std::min<int64_t>(n_sets_local, (int64_t)16 << 20) : n_sets_local;
+  // nranks = 0: no communicator; else the greedy all-gathers per-rank batches
+  const int64_t cap = nranks > 0 ? std::min<int64_t>(n_sets_local, (int64_t)16 << 20) : n_sets_local;
   w.batch_cap = cap;
-  const int64_t gathered = nranks > 1 ? cap * nranks : 0;
+  const int64_t gathered = nranks > 0 ? cap * nranks : 0;
   w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);
   w.gath_sorted = (unsigned long long*)take((size_t)gathered * 8 + 8);
-  const int64_t list_max = std::max<int64_t>(nranks > 1 ? gathered : n_sets_local, 1);
+  const int64_t list_max = std::max<int64_t>(nranks > 0 ? gathered : n_sets_local, 1);
   w.sort_tmp_bytes = std::max(sort_temp_bytes(list_max), select_temp_bytes(list_max));
   w.sort_tmp = take(w.sort_tmp_bytes);
   w.bytes = off;
@@ -470,7 +471,7 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
   if (!h || !bytes || n_jobs < 0) return fail(h, COSCHED_E_ARG, "bad workspace_size arguments");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  *bytes = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, nullptr, nullptr);
+  *bytes = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 0, nullptr, nullptr);
   return COSCHED_OK;
 }
 
@@ -497,7 +498,7 @@ cosched_status cosched_set_comm(cosched_t h, const void* uid, int rank, int nran
     h->comm = nullptr;
   }
   h->scored = false;
-  if (nranks == 1) {
+  if (nranks == 1 && !uid) {  // single process without NCCL
     h->rank = 0;
     h->nranks = 1;
     h->view_nranks = 1;
@@ -530,7 +531,7 @@ cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks) {
 }
 
 static cosched_status allreduce_op(cosched_t h, void* dev, size_t count, int dtype, int op) {
-  if (h->nranks <= 1 || !h->comm) return COSCHED_OK;
+  if (!h->comm) return COSCHED_OK;
   int r = g_nccl.allReduce(dev, dev, count, dtype, op, h->comm, h->stream);
   if (r != 0)
     return fail(h, COSCHED_E_NCCL, std::string("ncclAllReduce: ") +
@@ -539,7 +540,7 @@ static cosched_status allreduce_op(cosched_t h, void* dev, size_t count, int dty
 }
 
 static cosched_status allreduce_max(cosched_t h, void* dev, size_t count, int dtype) {
-  if (h->nranks <= 1 || !h->comm) return COSCHED_OK;
+  if (!h->comm) return COSCHED_OK;
   int r = g_nccl.allReduce(dev, dev, count, dtype, kNcclMax, h->comm, h->stream);
   if (r != 0)
     return fail(h, COSCHED_E_NCCL, std::string("ncclAllReduce: ") +
@@ -559,7 +560,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     return fail(h, COSCHED_E_ARG, "queue too large: more than 2^32-2 sets");
   int64_t first, count;
   shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
-  size_t need = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, nullptr, nullptr);
+  size_t need = workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 0, nullptr, nullptr);
   if (!workspace_dev || workspace_bytes < need || ((uintptr_t)workspace_dev & 255))
     return fail(h, COSCHED_E_OOM, "workspace missing, misaligned or smaller than cosched_workspace_size");
   float* obj = nullptr;
@@ -573,7 +574,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   DeviceGuard g(h->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Workspace ws;
-  workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 1, (char*)workspace_dev, &ws);
+  workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 0, (char*)workspace_dev, &ws);
   h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
   launch_fill_u64(ws.err, ~0ull, 1, st);
@@ -793,7 +794,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     const unsigned long long* list = (const unsigned long long*)ws.alive;
     unsigned long long* sorted = (unsigned long long*)ws.alive2;
     int64_t m = nk;
-    if (W > 1) {
+    if (h->comm) {  // every rank scans the same gathered list (also with a 1-rank communicator)
       int64_t mx = nk;
       CK(cudaMemcpyAsync(ws.counters + 4, &mx, 8, cudaMemcpyHostToDevice, s));
       st = allreduce_op(h, ws.counters + 4, 1, kNcclUint64, kNcclMax);
@@ -816,7 +817,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     // scan the sorted list in chunks; between chunks drop (order-preserving)
     // every key whose set touches a job taken meanwhile
     unsigned long long* cur = sorted;
-    unsigned long long* spare = (W > 1) ? ws.gath : (unsigned long long*)ws.alive;
+    unsigned long long* spare = h->comm ? ws.gath : (unsigned long long*)ws.alive;
     const int64_t kChunk = getenv("COSCHED_GREEDY_CHUNK") ? atoll(getenv("COSCHED_GREEDY_CHUNK")) : (1 << 18);
     while (m > 0 && n_picks < k) {
       const int64_t len = std::min<int64_t>(m, kChunk);

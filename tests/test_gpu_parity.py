@@ -323,3 +323,28 @@ def test_fast_scorer_equals_generic(cs, n_slots, n):
     same = (cfg0 == cfg1) & ((obj0 == obj1) | ((cfg0 < 0) & (cfg1 < 0)))
     assert same.mean() >= 1 - 1e-6, (np.nonzero(~same)[0][:10], cfg0[~same][:10], cfg1[~same][:10])
     assert s0.local_best_key() == s1.local_best_key()
+
+
+def test_one_rank_nccl_communicator_matches_no_comm(cs):
+    """Every collective path (best-set u64 max all-reduce, greedy min/max + histogram
+    all-reduces and per-batch all-gathers) run through a real one-rank NCCL communicator
+    returns exactly what the communicator-free path returns."""
+    for name, k in (("C3", 500), ("C2", 4)):
+        pb, F = bench_config(name)
+        a = cs.Scheduler(pb)
+        b = cs.Scheduler(pb)
+        b.set_comm(cs.get_unique_id(), 0, 1)
+        Fd = torch.from_numpy(F).cuda()
+        oa, ca = a.score_all(Fd)
+        ob, cb = b.score_all(Fd)
+        torch.cuda.synchronize()
+        assert torch.equal(ca, cb) and torch.equal(oa, ob)
+        assert a.best_set() == b.best_set()
+        assert a.best_allocation(k) == b.best_allocation(k)
+    pb = make_problem("b200_3way", "c21", coef_seed=11, alpha=0.2)
+    F, _ = make_features(60, seed=11)
+    a, b = cs.Scheduler(pb), cs.Scheduler(pb)
+    b.set_comm(cs.get_unique_id(), 0, 1)
+    for s in (a, b):
+        s.score_all(torch.from_numpy(F).cuda())
+    assert a.best_allocation(20) == b.best_allocation(20)
