@@ -224,6 +224,50 @@ cosched_status cosched_set_search(cosched_t h, int mode, int32_t start_state, in
  * the climbs (revisits included) for hill climbing. Synchronises. */
 cosched_status cosched_last_search_evals(cosched_t h, int64_t* evals);
 
+/* ---- Worst / proposal / best against a ground truth ----
+ *
+ * The paper's evaluation: for every set of the last
+ * cosched_score_all, the PROPOSAL (the scored cfg) is re-scored by a
+ * ground-truth performance model, and BEST / WORST are the largest / smallest
+ * ground-truth objective over the configs whose ground-truth Fairness exceeds
+ * alpha. The ground truth is SPEC.md's synthetic GPU (`true_rperf`; reading
+ * R21) with these constants -- the stand-in for the paper's A100 measurements. */
+typedef struct {
+  int32_t g_full;        /* GPCs of the unpartitioned chip (the normalisation point) */
+  int32_t n_modules;     /* memory modules of the chip */
+  int32_t modules[17];   /* private option: modules given to g GPCs, g = 0..16 */
+  float w_base, w_gpc;   /* static power and power per GPC at full non-tensor compute (W) */
+  float kappa, f_min;    /* tensor power multiplier; minimum throttle factor */
+  float p_max;           /* cap of the normalisation run (W) */
+} cosched_truth_desc;
+
+typedef struct {
+  float* prop_obj;   /* device [n_sets_local] ground-truth objective of the proposal (-inf: no proposal) */
+  float* prop_fair;  /* device [n_sets_local] its ground-truth Fairness */
+  float* best_obj;   /* device [n_sets_local] best ground-truth objective with true Fairness > alpha (-inf: none) */
+  float* worst_obj;  /* device [n_sets_local] worst such objective (-inf: none) */
+} cosched_eval_out;
+
+typedef struct {
+  int64_t n_compared;            /* sets with a proposal and a truly feasible config (all ranks) */
+  int64_t n_violations;          /* of those, proposals whose true Fairness <= alpha */
+  double geomean_prop_over_best; /* geometric mean over the compared sets of proposal / best */
+  double geomean_worst_over_best;
+} cosched_eval_summary;
+
+/* Workspace bytes for cosched_evaluate_truth on this rank's shard. */
+cosched_status cosched_evaluate_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes);
+
+/* COLLECTIVE (sums the summary over ranks). Requires cosched_score_all with out
+ * != NULL; features / jobs must be the ones it scored. Outputs are for this
+ * rank's shard; every member of out must be non-NULL. Synchronises the stream. COSCHED_E_ARG for
+ * invalid constants (g_full < 1 or > 16, n_modules < 1, p_max <= 0,
+ * f_min outside (0, 1], a state's GPCs > g_full). */
+cosched_status cosched_evaluate_truth(cosched_t h, const cosched_truth_desc* truth, const float* features_dev,
+                                      int64_t n_rows, const int32_t* jobs_dev, void* workspace,
+                                      size_t workspace_bytes, const cosched_eval_out* out,
+                                      cosched_eval_summary* summary, void* cuda_stream);
+
 /* Device time (ms, CUDA events on the caller's stream) of the last
  * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */

@@ -105,6 +105,7 @@ class Scheduler:
         self._ws = None
         self._out = None
         self.n_jobs = 0
+        self.first, self.count = 0, 0
 
     def close(self):
         if getattr(self, "_h", None):
@@ -221,6 +222,32 @@ class Scheduler:
         return {"status": st, "cfg": cfg.value, "state": cfg.value // self.n_caps if cfg.value >= 0 else -1,
                 "cap": cfg.value % self.n_caps if cfg.value >= 0 else -1, "obj": obj.value,
                 "rperf": [rp[i] for i in range(self.n_slots)], "throughput": thr.value, "fairness": fair.value}
+
+    def evaluate_truth(self, features, truth, jobs=None, stream=None):
+        """Worst / proposal / best of the last score_all under a ground-truth model (NEXT #3).
+        truth: any object with g_full, n_modules, modules (mapping GPCs -> modules), w_base,
+        w_gpc, kappa, f_min, p_max. Returns (prop_obj, prop_fair, best_obj, worst_obj) device
+        tensors of the shard and a summary dict (collective with a communicator)."""
+        import torch
+        dev = features.device
+        mods = (ctypes.c_int32 * 17)(*[int(truth.modules.get(g, 0)) for g in range(17)])
+        d = _lib.TruthDesc(int(truth.g_full), int(truth.n_modules), mods, float(truth.w_base), float(truth.w_gpc),
+                           float(truth.kappa), float(truth.f_min), float(truth.p_max))
+        b = ctypes.c_size_t()
+        self._check(self._L.cosched_evaluate_workspace_size(self._h, self.n_jobs, ctypes.byref(b)))
+        ws = torch.empty(b.value + 256, dtype=torch.uint8, device=dev)
+        wp = (ws.data_ptr() + 255) & ~255
+        n = max(self.count, 1)
+        outs = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(4)]
+        o = _lib.EvalOut(*[t.data_ptr() for t in outs])
+        sm = _lib.EvalSummary()
+        self._check(self._L.cosched_evaluate_truth(self._h, ctypes.byref(d), features.data_ptr(), features.shape[0],
+                                                   None if jobs is None else jobs.data_ptr(), wp, b.value,
+                                                   ctypes.byref(o), ctypes.byref(sm), _stream_handle(stream)))
+        summary = {"n_compared": sm.n_compared, "n_violations": sm.n_violations,
+                   "geomean_prop_over_best": sm.geomean_prop_over_best,
+                   "geomean_worst_over_best": sm.geomean_worst_over_best}
+        return tuple(t[:self.count] for t in outs), summary
 
     def best_allocation(self, k: int):
         """(status, set_ids, cfgs, total_obj); collective when a communicator is set."""

@@ -48,6 +48,22 @@ class FitOut(ctypes.Structure):
                 ("count", ctypes.c_void_p), ("rms", ctypes.c_void_p)]
 
 
+class TruthDesc(ctypes.Structure):
+    _fields_ = [("g_full", ctypes.c_int32), ("n_modules", ctypes.c_int32), ("modules", ctypes.c_int32 * 17),
+                ("w_base", ctypes.c_float), ("w_gpc", ctypes.c_float), ("kappa", ctypes.c_float),
+                ("f_min", ctypes.c_float), ("p_max", ctypes.c_float)]
+
+
+class EvalOut(ctypes.Structure):
+    _fields_ = [("prop_obj", ctypes.c_void_p), ("prop_fair", ctypes.c_void_p), ("best_obj", ctypes.c_void_p),
+                ("worst_obj", ctypes.c_void_p)]
+
+
+class EvalSummary(ctypes.Structure):
+    _fields_ = [("n_compared", ctypes.c_int64), ("n_violations", ctypes.c_int64),
+                ("geomean_prop_over_best", ctypes.c_double), ("geomean_worst_over_best", ctypes.c_double)]
+
+
 FIT_OK, FIT_NO_SAMPLES, FIT_INSUFFICIENT, FIT_RANK_DEFICIENT, FIT_MISSING_C = 0, 1, 2, 3, 4
 
 # (name, restype, argtypes) for every symbol include/cosched.h declares
@@ -79,6 +95,9 @@ SIGNATURES = [
     ("cosched_last_timings", I32, [P, P]),
     ("cosched_kernel_launches", I64, [P]),
     ("cosched_last_greedy_rounds", I64, [P]),
+    ("cosched_evaluate_workspace_size", I32, [P, I64, P]),
+    ("cosched_evaluate_truth", I32, [P, ctypes.POINTER(TruthDesc), P, I64, P, P, ctypes.c_size_t,
+                                     ctypes.POINTER(EvalOut), ctypes.POINTER(EvalSummary), P]),
     ("cosched_fit_workspace_size", I32, [ctypes.POINTER(FitDesc), P]),
     ("cosched_fit", I32, [ctypes.POINTER(FitDesc), P, ctypes.c_size_t, ctypes.POINTER(FitOut), P]),
     ("cosched_fit_last_error", ctypes.c_char_p, []),

@@ -26,7 +26,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct {
   char internal[128];
 } ncclUniqueId;
-enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
+enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 struct NcclApi {
   bool tried = false;
   void* lib = nullptr;
@@ -105,6 +105,10 @@ struct cosched_ctx {
   int view_nranks = 1;  // shard view without comm (tests)
   int64_t greedy_rounds = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // host copies of the table (ground-truth evaluation)
+  std::vector<int32_t> h_gpcs, h_mem;
+  std::vector<float> h_caps;
+  double* d_sums = nullptr;  // [4] ground-truth summary sums
   static constexpr int kSmallSets = 512;
   static constexpr int kDetailRows = 8192;
 };
@@ -290,6 +294,9 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
   h->device = cuda_device;
   h->n_slots = d->n_slots;
   h->objective = d->objective;
+  h->h_gpcs.assign(d->state_gpcs, d->state_gpcs + (size_t)d->n_states * d->n_slots);
+  h->h_mem.assign(d->state_mem, d->state_mem + d->n_states);
+  h->h_caps.assign(d->caps_w, d->caps_w + d->n_caps);
   SpaceParams& sp = h->sp;
   sp.n_slots = d->n_slots;
   sp.n_states = d->n_states;
@@ -324,7 +331,7 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
             cudaMalloc(&h->d_small_ids, 64 * 8) == cudaSuccess &&
             cudaMalloc(&h->d_detail, (size_t)cosched_ctx::kDetailRows * 8 * 4) == cudaSuccess &&
             cudaMalloc(&h->d_detail_ids, (size_t)cosched_ctx::kDetailRows * 8) == cudaSuccess &&
-            cudaMallocHost(&h->h_pinned, 8 * 8) == cudaSuccess &&
+            cudaMallocHost(&h->h_pinned, 8 * 8) == cudaSuccess && cudaMalloc(&h->d_sums, 4 * 8) == cudaSuccess &&
             cudaEventCreate(&h->ev[0]) == cudaSuccess && cudaEventCreate(&h->ev[1]) == cudaSuccess &&
             cudaEventCreate(&h->ev[2]) == cudaSuccess && cudaEventCreate(&h->ev[3]) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_c, d->coef_c, nc * 6 * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -351,6 +358,7 @@ void cosched_destroy(cosched_t h) {
     cudaFree(h->d_small_ids);
     cudaFree(h->d_detail);
     cudaFree(h->d_detail_ids);
+    cudaFree(h->d_sums);
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
     for (int i = 0; i < 4; i++)
       if (h->ev[i]) cudaEventDestroy(h->ev[i]);
@@ -1055,6 +1063,53 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
   }
   if (total_obj) *total_obj = tot;
   if (n_found) *n_found = (int32_t)take;
+  return COSCHED_OK;
+}
+
+// ---- worst / proposal / best against a ground truth (truth.cu) ------------------------
+cosched_status cosched_evaluate_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes) {
+  if (!h || !bytes || n_jobs < 0) return COSCHED_E_ARG;
+  int64_t first, count;
+  shard_bounds(n_jobs, h->n_slots, h->rank, h->comm ? h->nranks : h->view_nranks, &first, &count);
+  *bytes = truth_workspace_bytes(n_jobs, count);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_evaluate_truth(cosched_t h, const cosched_truth_desc* truth, const float* features_dev,
+                                      int64_t n_rows, const int32_t* jobs_dev, void* workspace,
+                                      size_t workspace_bytes, const cosched_eval_out* out,
+                                      cosched_eval_summary* summary, void* cuda_stream) {
+  if (!h) return COSCHED_E_ARG;
+  if (!truth || !features_dev || !out || !out->prop_obj || !out->prop_fair || !out->best_obj || !out->worst_obj)
+    return fail(h, COSCHED_E_ARG, "null argument");
+  if (!h->scored || !h->out_cfg) return fail(h, COSCHED_E_STATE, "call cosched_score_all with out first");
+  if (truth->g_full < 1 || truth->g_full > 16 || truth->n_modules < 1 || !(truth->p_max > 0.0f) ||
+      !(truth->f_min > 0.0f && truth->f_min <= 1.0f) || !(truth->w_gpc >= 0.0f) || !(truth->kappa >= 0.0f))
+    return fail(h, COSCHED_E_ARG, "invalid ground-truth constants");
+  for (int32_t g : h->h_gpcs)
+    if (g > truth->g_full) return fail(h, COSCHED_E_ARG, "a state gives more GPCs than g_full");
+  if (!workspace || workspace_bytes < truth_workspace_bytes(h->n_jobs, h->n_sets))
+    return fail(h, COSCHED_E_OOM, "workspace too small");
+  (void)n_rows;
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int n = truth_enqueue(truth, h->sp, h->objective, h->h_gpcs.data(), h->h_mem.data(), h->h_caps.data(), features_dev,
+                        jobs_dev, h->n_jobs, h->first, h->n_sets, h->out_cfg, out, workspace, h->d_sums, st);
+  if (n < 0) return cuda_fail(h, cudaGetLastError(), "evaluate_truth launch");
+  h->launches += n;
+  if (h->comm) {
+    int r = g_nccl.allReduce(h->d_sums, h->d_sums, 4, kNcclFloat64, kNcclSum, h->comm, st);
+    if (r != 0) return fail(h, COSCHED_E_NCCL, "ncclAllReduce (evaluate_truth)");
+  }
+  double sums[4];
+  CK(cudaMemcpyAsync(sums, h->d_sums, sizeof sums, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (summary) {
+    summary->n_compared = (int64_t)llround(sums[0]);
+    summary->n_violations = (int64_t)llround(sums[3]);
+    summary->geomean_prop_over_best = sums[0] > 0 ? exp(sums[1] / sums[0]) : nan("");
+    summary->geomean_worst_over_best = sums[0] > 0 ? exp(sums[2] / sums[0]) : nan("");
+  }
   return COSCHED_OK;
 }
 

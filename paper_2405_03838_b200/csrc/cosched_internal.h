@@ -118,6 +118,12 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
                                uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
                                cudaStream_t st);
 int64_t pad_jobs(int64_t n_jobs);
+// truth.cu
+size_t truth_workspace_bytes(int64_t n_jobs, int64_t count);
+int truth_enqueue(const cosched_truth_desc* d, const SpaceParams& sp, int objective, const int32_t* gpcs,
+                  const int32_t* mem, const float* caps, const float* features, const int32_t* jobs, int64_t n_jobs,
+                  int64_t first, int64_t count, const int32_t* prop_cfg, const cosched_eval_out* out, void* workspace,
+                  double* sums_dev, cudaStream_t st);
 // calib.cu
 cosched_status fit_validate_desc(const cosched_fit_desc* d);
 size_t fit_workspace_bytes(const cosched_fit_desc* d);
