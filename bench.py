@@ -19,6 +19,7 @@ metric is quoted on; synthetic class-shaped inputs (synth/).
 from __future__ import annotations
 
 import argparse
+import copy
 import json
 import math
 import os
@@ -229,6 +230,25 @@ def calibration_metrics(pb, F, dev, args):
         times.append(e0.elapsed_time(e1))
     ms = statistics.median(times)
     st = r.status.cpu().numpy()
+    # the paper's workflow on the fitted table (NEXT #3): search the queue, evaluate the
+    # proposals against the ground truth (worst / proposal / best geometric means)
+    from synth.ground_truth import B200 as truth
+    pbf = copy.copy(pb)
+    pbf.coef_c = r.coef_c.cpu().numpy().astype(np.float32)
+    pbf.coef_d = r.coef_d.cpu().numpy().astype(np.float32)
+    sf = cs.Scheduler(pbf, device=dev.index or 0)
+    Fd = targs[0]
+    sf.score_all(Fd)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _, summ = sf.evaluate_truth(Fd, truth)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pipeline = dict(summ)
+    pipeline["evaluate_ms"] = e0.elapsed_time(e1)
+    pipeline["note"] = ("C, D fitted on the synthetic GPU; the fitted table searched over the queue; proposals "
+                        "scored by the ground truth (PAPER.md L752/L777 analogue)")
+    sf.close()
     n_solo, n_co = len(ts.solo_app), len(ts.co_app)
     npart = ts.co_partners.shape[1] if n_co else 0
     # algorithmic bytes: each sample record once (app, key, rperf, partners) + each app's counters
@@ -241,7 +261,8 @@ def calibration_metrics(pb, F, dev, args):
             "corun_samples": n_co, "ms": ms, "samples_per_s": (n_solo + n_co) / (ms * 1e-3),
             "keys_fitted": [int((st[:, 0] == 0).sum()), int((st[:, 1] == 0).sum())],
             "algorithmic_bytes": algo, "achieved_gbs": gbs, "hbm_peak_gbs": peaks.get("hbm_gbs"),
-            "hbm_frac": gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None, "peak_source": src}
+            "hbm_frac": gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None, "peak_source": src,
+            "pipeline": pipeline}
 
 
 def hill_metrics(sched, Fd, pb, stream, args):
