@@ -268,6 +268,27 @@ cosched_status cosched_evaluate_truth(cosched_t h, const cosched_truth_desc* tru
                                       size_t workspace_bytes, const cosched_eval_out* out,
                                       cosched_eval_summary* summary, void* cuda_stream);
 
+/* ---- Node-level power budgeting ----------------------
+ *
+ * The job manager's power budgeting ("sets the power caps", L400, L782,
+ * L844): the n_gpus GPUs are grouped into nodes of gpus_per_node consecutive
+ * entries, GPU g running set set_ids[g] (e.g. from cosched_best_allocation).
+ * Per GPU and cap, thr(p) = the best Throughput over the states whose Fairness
+ * > alpha (lowest state on ties); per node one cap per GPU maximising
+ *   objective 1: sum_g thr_g(p_g)                 s.t. sum_g P(p_g) <= node_power_w
+ *   objective 2: sum_g thr_g(p_g) / sum_g P(p_g)  s.t. the same
+ * exactly, by a DP over the total power in units of the caps' gcd (reading
+ * R23; caps must be integer watts, node_power_w / gcd <= 12287). Uses the
+ * projection of the last cosched_score_all (any rank: every rank projects the
+ * whole queue; no collective). Outputs (host): caps_out[n_gpus] cap index,
+ * cfgs_out[n_gpus] = state * n_caps + cap, node_obj[n_nodes]; a node with no
+ * feasible assignment gets -1 / -1 / -inf. Synchronises the stream. */
+cosched_status cosched_node_workspace_size(cosched_t h, int64_t n_gpus, int32_t gpus_per_node, double node_power_w,
+                                           size_t* bytes);
+cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* set_ids, int32_t gpus_per_node,
+                                   double node_power_w, int32_t objective, void* workspace, size_t workspace_bytes,
+                                   int32_t* caps_out, int32_t* cfgs_out, float* node_obj, void* cuda_stream);
+
 /* Device time (ms, CUDA events on the caller's stream) of the last
  * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */

@@ -223,6 +223,26 @@ class Scheduler:
                 "cap": cfg.value % self.n_caps if cfg.value >= 0 else -1, "obj": obj.value,
                 "rperf": [rp[i] for i in range(self.n_slots)], "throughput": thr.value, "fairness": fair.value}
 
+    def node_budget(self, set_ids: Sequence[int], gpus_per_node: int, node_power_w: float, objective: int,
+                    stream=None):
+        """Per-node power caps for the GPUs running set_ids (NEXT #4, reading R23).
+        Returns (caps, cfgs, node_obj) host lists."""
+        import torch
+        n = len(set_ids)
+        b = ctypes.c_size_t()
+        self._check(self._L.cosched_node_workspace_size(self._h, n, gpus_per_node, float(node_power_w),
+                                                        ctypes.byref(b)))
+        ws = torch.empty(b.value + 256, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        wp = (ws.data_ptr() + 255) & ~255
+        ids = (ctypes.c_int64 * n)(*[int(x) for x in set_ids])
+        caps = (ctypes.c_int32 * n)()
+        cfgs = (ctypes.c_int32 * n)()
+        nodes = max(n // max(gpus_per_node, 1), 1)
+        obj = (ctypes.c_float * nodes)()
+        self._check(self._L.cosched_node_budget(self._h, n, ids, gpus_per_node, float(node_power_w), objective, wp,
+                                                b.value, caps, cfgs, obj, _stream_handle(stream)))
+        return list(caps), list(cfgs), [obj[i] for i in range(n // gpus_per_node)]
+
     def evaluate_truth(self, features, truth, jobs=None, stream=None):
         """Worst / proposal / best of the last score_all under a ground-truth model (NEXT #3).
         truth: any object with g_full, n_modules, modules (mapping GPCs -> modules), w_base,

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcosched.so")
-SOURCES = ["api.cu", "kernels.cu", "score_pairs.cu", "score_triples.cu", "greedy.cu", "calib.cu", "truth.cu"]
+SOURCES = ["api.cu", "kernels.cu", "score_pairs.cu", "score_triples.cu", "greedy.cu", "calib.cu", "truth.cu", "node.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

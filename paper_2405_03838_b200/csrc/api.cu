@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -1063,6 +1064,70 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
   }
   if (total_obj) *total_obj = tot;
   if (n_found) *n_found = (int32_t)take;
+  return COSCHED_OK;
+}
+
+// ---- node-level power budgeting (node.cu) ---------------------------------------------
+static cosched_status node_units(cosched_t h, int32_t gpus_per_node, double node_power_w, int32_t* U, float* unit,
+                                 std::vector<int32_t>* u) {
+  long long g = 0;
+  std::vector<long long> w(h->h_caps.size());
+  for (size_t i = 0; i < h->h_caps.size(); i++) {
+    const double c = h->h_caps[i];
+    if (c != floor(c) || c < 1) return fail(h, COSCHED_E_ARG, "node budgeting needs integer-watt caps");
+    w[i] = (long long)c;
+    g = std::gcd(g, w[i]);
+  }
+  if (!(node_power_w >= 0) || gpus_per_node < 1 || gpus_per_node > 64)
+    return fail(h, COSCHED_E_ARG, "bad node budget or gpus_per_node");
+  const double units = floor(node_power_w / (double)g + 1e-9);
+  if (units > 12287) return fail(h, COSCHED_E_ARG, "node_power_w / gcd(caps) exceeds 12287 budget units");
+  *U = (int32_t)units;
+  *unit = (float)g;
+  u->resize(w.size());
+  for (size_t i = 0; i < w.size(); i++) (*u)[i] = (int32_t)(w[i] / g);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_node_workspace_size(cosched_t h, int64_t n_gpus, int32_t gpus_per_node, double node_power_w,
+                                           size_t* bytes) {
+  if (!h || !bytes || n_gpus < 1) return COSCHED_E_ARG;
+  int32_t U;
+  float unit;
+  std::vector<int32_t> u;
+  cosched_status st = node_units(h, gpus_per_node, node_power_w, &U, &unit, &u);
+  if (st != COSCHED_OK) return st;
+  *bytes = node_workspace_bytes(n_gpus, h->sp.n_caps, U, gpus_per_node);
+  return COSCHED_OK;
+}
+
+cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* set_ids, int32_t gpus_per_node,
+                                   double node_power_w, int32_t objective, void* workspace, size_t workspace_bytes,
+                                   int32_t* caps_out, int32_t* cfgs_out, float* node_obj, void* cuda_stream) {
+  if (!h) return COSCHED_E_ARG;
+  if (n_gpus < 1 || !set_ids || !caps_out || !cfgs_out || !node_obj || gpus_per_node < 1 ||
+      n_gpus % gpus_per_node != 0 || (objective != 1 && objective != 2))
+    return fail(h, COSCHED_E_ARG, "bad node budgeting arguments (n_gpus must be a multiple of gpus_per_node)");
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  const int64_t total = cosched::n_sets(h->n_jobs, h->n_slots);
+  for (int64_t g = 0; g < n_gpus; g++)
+    if (set_ids[g] < 0 || set_ids[g] >= total) return fail(h, COSCHED_E_ARG, "set id out of range");
+  int32_t U;
+  float unit;
+  std::vector<int32_t> u;
+  cosched_status st = node_units(h, gpus_per_node, node_power_w, &U, &unit, &u);
+  if (st != COSCHED_OK) return st;
+  if (!workspace || workspace_bytes < node_workspace_bytes(n_gpus, h->sp.n_caps, U, gpus_per_node))
+    return fail(h, COSCHED_E_OOM, "workspace too small");
+  st = check_deferred(h);
+  if (st != COSCHED_OK) return st;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  int n = node_enqueue(h->sp, h->ws.ka, h->ws.kb, h->ws.w, set_ids, n_gpus, gpus_per_node, U, unit, u.data(),
+                       objective, workspace, caps_out, cfgs_out, node_obj, s);
+  if (n < 0) return cuda_fail(h, cudaGetLastError(), "node_budget launch");
+  h->launches += n;
+  CK(cudaStreamSynchronize(s));
   return COSCHED_OK;
 }
 

@@ -118,6 +118,11 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
                                uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
                                cudaStream_t st);
 int64_t pad_jobs(int64_t n_jobs);
+// node.cu
+size_t node_workspace_bytes(int64_t n_gpus, int32_t n_caps, int32_t U, int32_t gpus_per_node);
+int node_enqueue(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids_host,
+                 int64_t n_gpus, int32_t gpus_per_node, int32_t U, float unit_w, const int32_t* u, int32_t objective,
+                 void* workspace, int32_t* caps_host, int32_t* cfg_host, float* node_obj_host, cudaStream_t st);
 // truth.cu
 size_t truth_workspace_bytes(int64_t n_jobs, int64_t count);
 int truth_enqueue(const cosched_truth_desc* d, const SpaceParams& sp, int objective, const int32_t* gpcs,
