@@ -387,6 +387,7 @@ def run_ours(args):
     # allocation latency (timed separately)
     alloc_ms = None
     alloc_rounds = None
+    node_info = None
     if args.alloc_k:
         sched.score_all(Fd, None, with_out=True, stream=stream)
         torch.cuda.synchronize()
@@ -394,6 +395,21 @@ def run_ours(args):
         st, ids, cfgs, tot = sched.best_allocation(args.alloc_k)
         alloc_ms = (time.perf_counter() - t0) * 1e3
         alloc_rounds = sched.greedy_rounds
+        # node-level power budgeting of the allocation (NEXT #4): nodes of 8 GPUs under
+        # a budget of 6 kW (75 % of 8 x P_max), caps per GPU by the exact knapsack DP
+        node_info = None
+        G = 8
+        if pb.n_slots >= 2 and len(ids) >= G:
+            use = ids[:len(ids) // G * G]
+            node_w = 0.75 * G * float(max(pb.caps_w))
+            sched.node_budget(use, G, node_w, pb.objective)  # warm
+            t1 = time.perf_counter()
+            caps_n, cfgs_n, nobj = sched.node_budget(use, G, node_w, pb.objective)
+            node_ms = (time.perf_counter() - t1) * 1e3
+            fin = [v for v in nobj if v > -math.inf]
+            node_info = {"nodes": len(nobj), "gpus_per_node": G, "node_budget_w": node_w, "ms": node_ms,
+                         "feasible_nodes": len(fin), "mean_node_objective": (sum(fin) / len(fin)) if fin else None,
+                         "mean_gpu_cap_w": float(np.mean([float(pb.caps_w[c]) for c in caps_n if c >= 0]))}
 
     if rank == 0:
         peaks, peak_src = _peaks()
@@ -435,6 +451,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": 8 + 32},
             "gpu_launches": int(launches),
             "prep_ms": statistics.mean(prep_ms), "allocation_ms": alloc_ms, "allocation_k": args.alloc_k, "allocation_rounds": alloc_rounds,
+            "node_budget": node_info,
             "clocks": clocks,
         }
         if args.hill:
