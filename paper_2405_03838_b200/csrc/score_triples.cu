@@ -91,6 +91,20 @@ __device__ __forceinline__ void issue_tstage(float* stage, uint64_t* bar, const 
                  fast + (((int64_t)(8 + k) * sp.n_stages + g) * sp.n_jobs_pad + j2) * kStageRS, rowb, bar);
 }
 
+// Partner partials of a landed stage, in place over its j1 blocks:
+// P1 -> [4], P0 -> [5], P2 -> [6], Q -> [7] (canonical order of eval_cfg<3>).
+__device__ __forceinline__ void tstage_partials(float* st) {
+  constexpr int rs = kStageRS, blk = kTT * kStageRS;
+  const float* rows = st + 8 * blk;
+  for (int e = threadIdx.x; e < blk; e += kTThreads) {
+    const int c = e % rs;
+    st[4 * blk + e] = __fadd_rn(st[4 * blk + e], rows[2 * rs + c]);  // P1 = ka[s1][j1] + kb[s1][j2]
+    st[5 * blk + e] = __fadd_rn(st[5 * blk + e], rows[1 * rs + c]);  // P0 = kb[s0][j1] + kb[s0][j2]
+    st[6 * blk + e] = __fadd_rn(rows[0 * rs + c], st[6 * blk + e]);  // P2 = ka[s2][j2] + kb[s2][j1]
+    st[7 * blk + e] = __uint_as_float(__float_as_uint(st[7 * blk + e]) + __float_as_uint(rows[3 * rs + c]));
+  }
+}
+
 }  // namespace
 
 template <int MINB>
@@ -132,6 +146,12 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   int s = 0, buf = 0;
   unsigned phase[2] = {0u, 0u};
   if (threadIdx.x == 0) issue_tstage(smem, &bars[0], sp, fast, A, B, J2, 0);
+  // stage pipeline: the partials of stage s+1 are built at the end of stage s,
+  // so one barrier per stage publishes them and frees the buffer of stage s
+  mbar_wait(&bars[0], phase[0]);
+  phase[0] ^= 1u;
+  tstage_partials(smem);
+  __syncthreads();
 
   float breg[kTM][kTM];
 #pragma unroll
@@ -150,23 +170,8 @@ __global__ void __launch_bounds__(kTThreads, MINB)
     const bool has_next = nt < g.n_tiles;
     if (has_next && threadIdx.x == 0)
       issue_tstage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nA, nB, nJ2, ns);
-    mbar_wait(&bars[buf], phase[buf]);
-    phase[buf] ^= 1u;
 
-    float* st = smem + buf * stage_floats;
-    // partner partials, in place over the j1 blocks: P1 -> [4], P0 -> [5], P2 -> [6], Q -> [7]
-    {
-      constexpr int blk = kTT * rs;
-      const float* rows = st + 8 * blk;
-      for (int e = threadIdx.x; e < blk; e += kTThreads) {
-        const int c = e % rs;
-        st[4 * blk + e] = __fadd_rn(st[4 * blk + e], rows[2 * rs + c]);  // P1 = ka[s1][j1] + kb[s1][j2]
-        st[5 * blk + e] = __fadd_rn(st[5 * blk + e], rows[1 * rs + c]);  // P0 = kb[s0][j1] + kb[s0][j2]
-        st[6 * blk + e] = __fadd_rn(rows[0 * rs + c], st[6 * blk + e]);  // P2 = ka[s2][j2] + kb[s2][j1]
-        st[7 * blk + e] = __uint_as_float(__float_as_uint(st[7 * blk + e]) + __float_as_uint(rows[3 * rs + c]));
-      }
-    }
-    __syncthreads();
+    float* st = smem + buf * stage_floats;  // landed, partials built (previous iteration)
 
     const float4* st4 = reinterpret_cast<const float4*>(st);
     constexpr int blk4 = kTT * rs4;
@@ -232,38 +237,60 @@ __global__ void __launch_bounds__(kTThreads, MINB)
           breg[a][b] = 0.0f;
         }
       __syncthreads();
-#pragma unroll 2
-      for (int e = threadIdx.x; e < kTT * kTT; e += kTThreads) {
-        const int rj = e >> 6, ri = e & 63;
-        const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
-        const int sg = sbg[rj * kTBgRow + ri];
-        const unsigned kbits = __float_as_uint(sbest[rj * kTBgRow + ri]);
-        sbg[rj * kTBgRow + ri] = -1;
-        if (!(j0 < j1 && j1 < j2 && j2 < g.n_jobs && j2 >= g.c0 && j2 < g.c1)) continue;
-        // never clipped (positive margins >= 8 > packed key, cosched_internal.h):
-        // the key's low bits give the argmax config; its exact FP32 objective
-        // in the canonical order w0 + (w1 + w2)
-        float bo = -INFINITY;
-        int bc = -1;
-        const int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
-        if (sg >= 0 && c < sp.n_cfg) {
-          const int st = c / sp.n_caps, p = c - st * sp.n_caps;
-          const float w0 = __ldg(w_row(w, sp, 0, st, j0) + p), w1 = __ldg(w_row(w, sp, 1, st, j1) + p),
-                      w2 = __ldg(w_row(w, sp, 2, st, j2) + p);
-          bo = __fadd_rn(w0, __fadd_rn(w1, w2));
-          bc = c;
+      // kPass sets per pass with all their loads in flight. Never clipped (positive
+      // margins >= 8 > packed key, cosched_internal.h): the key's low bits give
+      // the argmax config; its exact FP32 objective in the canonical order
+      // w0 + (w1 + w2)
+      constexpr int kPass = 4;
+#pragma unroll 1
+      for (int e0 = 0; e0 < kTT * kTT; e0 += kPass * kTThreads) {
+        float f0[kPass], f1[kPass], f2[kPass];
+        int c_[kPass];
+#pragma unroll
+        for (int u = 0; u < kPass; u++) {
+          const int e = e0 + u * kTThreads + threadIdx.x;
+          const int rj = e >> 6, ri = e & 63;
+          const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
+          const int sg = sbg[rj * kTBgRow + ri];
+          const unsigned kbits = __float_as_uint(sbest[rj * kTBgRow + ri]);
+          sbg[rj * kTBgRow + ri] = -1;  // every slot, valid or not
+          const bool ok = j0 < j1 && j1 < j2 && j2 < g.n_jobs && j2 >= g.c0 && j2 < g.c1;
+          const int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
+          c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
+          f0[u] = f1[u] = f2[u] = 0.0f;
+          if (c_[u] >= 0) {
+            const int st_ = c / sp.n_caps, p = c - st_ * sp.n_caps;
+            f0[u] = __ldg(w_row(w, sp, 0, st_, j0) + p);
+            f1[u] = __ldg(w_row(w, sp, 1, st_, j1) + p);
+            f2[u] = __ldg(w_row(w, sp, 2, st_, j2) + p);
+          }
         }
-        const int64_t sid = j2 * (j2 - 1) * (j2 - 2) / 6 + j1 * (j1 - 1) / 2 + j0;
-        const int64_t k = sid - g.first_set;
-        if (out_obj) out_obj[k] = bo;
-        if (out_cfg) out_cfg[k] = bc;
-        if (bc >= 0) {
-          const unsigned long long kk = pack_key(bo, sid);
-          key = kk > key ? kk : key;
+#pragma unroll
+        for (int u = 0; u < kPass; u++) {
+          if (c_[u] == -2) continue;
+          const int e = e0 + u * kTThreads + threadIdx.x;
+          const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0
+          const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
+          const int bc = c_[u];
+          const float bo = bc >= 0 ? __fadd_rn(f0[u], __fadd_rn(f1[u], f2[u])) : -INFINITY;
+          const int64_t sid = j2 * (j2 - 1) * (j2 - 2) / 6 + j1 * (j1 - 1) / 2 + j0;
+          const int64_t k = sid - g.first_set;
+          if (out_obj) out_obj[k] = bo;
+          if (out_cfg) out_cfg[k] = bc;
+          if (bc >= 0) {
+            const unsigned long long kk = pack_key(bo, sid);
+            key = kk > key ? kk : key;
+          }
         }
       }
     }
 
+    // next stage: wait for its data and build its partials before the barrier
+    if (has_next) {
+      mbar_wait(&bars[buf ^ 1], phase[buf ^ 1]);
+      phase[buf ^ 1] ^= 1u;
+      tstage_partials(smem + (buf ^ 1) * stage_floats);
+    }
     __syncthreads();
     if (!has_next) break;
     t = nt;
