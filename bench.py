@@ -180,19 +180,22 @@ def run_reference(args):
     from synth import bench_config
     pb, F = bench_config(args.config)
     n_slots = pb.n_slots
-    # bounded sample per step, sized so the whole run stays within a few minutes
-    for _ in range(args.warmup):
-        pass
+    # bounded sample per step, sized so the whole run stays within a few minutes;
+    # warm-up steps are short untimed samples (process start-up, page-in)
+    for k in range(args.warmup):
+        cpu_oracle_rate(pb, F, n_slots, budget_s=0.5, first=k * 104729)
     steps = []
     info = None
     for k in range(args.steps):
         info = cpu_oracle_rate(pb, F, n_slots, budget_s=args.ref_budget, first=k * 7919)
         steps.append(info["value"])
     value = statistics.median(steps)
-    n_cand_step = None
+    import oracle
+    n_cand_step = oracle.n_sets(int(F.shape[0]), n_slots) * pb.n_configs
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": n_cand_step / value * 1e3,  # the whole workload at the sampled rate
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n_jobs": int(F.shape[0]), "n_slots": n_slots,
                        "n_configs": pb.n_configs, "table": pb.name, "objective": pb.objective,
                        "alpha": pb.alpha, "parallelism": "host processes"},
