@@ -617,10 +617,16 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   return COSCHED_OK;
 }
 
+static cosched_status deferred_status(cosched_t h, unsigned long long e);
+
 static cosched_status check_deferred(cosched_t h) {
   CK(cudaMemcpyAsync(h->h_pinned, h->ws.err, 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  unsigned long long e = h->h_pinned[0];
+  return deferred_status(h, h->h_pinned[0]);
+}
+
+// the validation outcome of the last score_all (err word written by k_validate)
+static cosched_status deferred_status(cosched_t h, unsigned long long e) {
   if (e == ~0ull) return COSCHED_OK;
   int code = (int)(e & 0xFF);
   long long pos = (long long)(e >> 8);
@@ -672,13 +678,19 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   if (!h) return COSCHED_E_ARG;
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
   DeviceGuard g(h->device);
-  cosched_status st = check_deferred(h);
+  // one device -> host round trip: all-reduce the key, decode the winner's config
+  // on the device, then read back the validation word, the key and the detail row
+  cosched_status st = allreduce_max(h, h->ws.best_key, 1, kNcclUint64);
   if (st != COSCHED_OK) return st;
-  st = allreduce_max(h, h->ws.best_key, 1, kNcclUint64);
-  if (st != COSCHED_OK) return st;
-  CK(cudaMemcpyAsync(h->h_pinned, h->ws.best_key, 8, cudaMemcpyDeviceToHost, h->stream));
+  launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->d_detail, h->stream);
+  h->launches++;
+  CK(cudaMemcpyAsync(h->h_pinned, h->ws.err, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->h_pinned + 1, h->ws.best_key, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->h_pinned + 2, h->d_detail, 8 * 4, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  uint64_t key = h->h_pinned[0];
+  st = deferred_status(h, h->h_pinned[0]);
+  if (st != COSCHED_OK) return st;
+  const uint64_t key = h->h_pinned[1];
   float o;
   int64_t sid;
   cosched_unpack_key(key, &o, &sid);
@@ -686,14 +698,7 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   if (obj) *obj = o;
   if (cfg) *cfg = -1;
   if (key == 0) return COSCHED_INFEASIBLE;
-  if (cfg) {
-    std::vector<float> rows;
-    st = detail_rows(h, &sid, 1, &rows);
-    if (st != COSCHED_OK) return st;
-    int32_t c;
-    memcpy(&c, &rows[0], 4);
-    *cfg = c;
-  }
+  if (cfg) memcpy(cfg, h->h_pinned + 2, 4);
   return COSCHED_OK;
 }
 

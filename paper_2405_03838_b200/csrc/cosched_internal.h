@@ -168,6 +168,9 @@ void launch_sort_keys_desc(const unsigned long long* keys, int64_t n, unsigned l
 void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
                         int64_t n,
                         float* out /* [n][4 + kMaxSlots] */, cudaStream_t st);
+// detail row of the set named by the device-resident packed key (best set)
+void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
+                        const unsigned long long* key, float* out, cudaStream_t st);
 void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive,
                            const uint32_t* taken, int64_t* alive_out, int64_t* n_out, cudaStream_t st);
 void launch_greedy_pairs_propose(const float* obj, int64_t first, int64_t c0, int64_t c1, const uint32_t* taken,

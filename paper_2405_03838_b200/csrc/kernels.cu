@@ -129,9 +129,11 @@ __device__ __forceinline__ float ka_value(const SpaceParams& sp, const CoefRow& 
 __device__ __forceinline__ float kb_value(const CoefRow& r, const float j[3]) {
   return flush_clamp(__fmul_rn(dot_v(r.d[0], j), kScale));
 }
-__device__ __forceinline__ float w_value(const SpaceParams& sp, const CoefRow& r, const float h[6], const float j[3]) {
+template <int NS>
+__device__ __forceinline__ float w_value(const CoefRow& r, const float h[6], const float j[3]) {
   float acc = dot_u(r.c, h);
-  for (int k = 0; k + 1 < sp.n_slots; k++) acc = __fadd_rn(acc, dot_v(r.d[k], j));
+#pragma unroll
+  for (int k = 0; k + 1 < NS; k++) acc = __fadd_rn(acc, dot_v(r.d[k], j));
   return __fmul_rn(acc, r.inv_p);
 }
 
@@ -144,10 +146,28 @@ __device__ __forceinline__ float w_value(const SpaceParams& sp, const CoefRow& r
 constexpr int kProjWarps = 4;
 constexpr int kProjJobs = 32 * kProjWarps;
 
+// A warp's 32 staged rows (row stride ld = cols + 1 floats) -> 32 consecutive
+// rows of `cols` floats in global memory: one flat coalesced copy, the (row,
+// col) of each element advanced incrementally (no division).
+__device__ __forceinline__ void flush_rows(const float* stg, int ld, int cols, float* __restrict__ dst, int lane) {
+  const int step_r = 32 / cols, step_c = 32 - step_r * cols;
+  int r = lane / cols, c = lane - r * cols;
+  for (int e = lane; e < 32 * cols; e += 32) {
+    dst[e] = stg[r * ld + c];
+    r += step_r;
+    c += step_c;
+    if (c >= cols) {
+      c -= cols;
+      r++;
+    }
+  }
+}
+
 // Grid (x: blocks of kProjJobs jobs, y: row kind): y < n_slices -> the ka and kb
 // rows of slice y; else the w row of (slot, state) = divmod(y - n_slices,
 // n_states). The per-slot min/max of w is reduced per block, then one atomic
-// per block.
+// per block. Block-uniform branches only; the cap loop has no per-element test.
+template <int NS>
 __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restrict__ hj, int64_t n_jobs,
                                                            const SpaceParams sp, const float* __restrict__ coef_c,
                                                            const float* __restrict__ coef_d,
@@ -156,7 +176,7 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
                                                            float* __restrict__ w, unsigned* wmm) {
   __shared__ CoefRow s_coef[kMaxCaps];
   __shared__ unsigned s_mm[2];
-  extern __shared__ float s_stage[];  // [kProjWarps][32][rs + 1]
+  extern __shared__ float s_stage[];  // [2][kProjWarps][32][rs + 1]
   const int y = blockIdx.y;
   const bool is_w = y >= sp.n_slices;
   const int slot = is_w ? (y - sp.n_slices) / sp.n_states : 0, state = is_w ? (y - sp.n_slices) % sp.n_states : 0;
@@ -174,41 +194,47 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
   __syncthreads();
   if (*err != ~0ull) return;  // invalid input: leave the workspace untouched (uniform per launch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rs = sp.rs, ld = rs + 1;
+  const int rs = sp.rs, ld = rs + 1, nc = sp.n_caps;
   const size_t npad = (size_t)sp.n_jobs_pad;
   const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
   unsigned lo = 0xFFFFFFFFu, hi = 0u;
   if (n0 < (int64_t)npad) {
-    float* stg = s_stage + warp * 32 * ld;
+    float* stg_a = s_stage + warp * 32 * ld;
+    float* stg_b = s_stage + (kProjWarps + warp) * 32 * ld;
+    float* row_a = stg_a + lane * ld;
+    float* row_b = stg_b + lane * ld;
     float h[6], j[3];
     const bool job = n < n_jobs;
     if (job) load_hj(hj, n, h, j);
-    const int passes = is_w ? 1 : 2;
-    for (int pass = 0; pass < passes; pass++) {
-      for (int p = 0; p < rs; p++) {
-        float v;
-        if (p >= sp.n_caps || !job) {
-          v = is_w ? -1e30f : kPadMargin;
-        } else {
+    if (!is_w) {
+      if (job) {
+        for (int p = 0; p < nc; p++) {
           const CoefRow& r = s_coef[p];
-          if (is_w) {
-            v = w_value(sp, r, h, j);
-            const unsigned uo = ord_float_d(v);
-            lo = uo < lo ? uo : lo;
-            hi = uo > hi ? uo : hi;
-          } else {
-            v = pass == 0 ? ka_value(sp, r, h) : kb_value(r, j);
-          }
+          row_a[p] = ka_value(sp, r, h);
+          row_b[p] = kb_value(r, j);
         }
-        stg[lane * ld + p] = v;
+      } else {
+        for (int p = 0; p < nc; p++) row_a[p] = row_b[p] = kPadMargin;
       }
+      for (int p = nc; p < rs; p++) row_a[p] = row_b[p] = kPadMargin;
       __syncwarp();
-      float* dst = (is_w ? w + ((size_t)slot * sp.n_states + state) * npad * rs
-                         : (pass == 0 ? ka : kb) + (size_t)y * npad * rs) +
-                   (size_t)n0 * rs;
-      for (int i = 0; i < 32; i++)
-        for (int p = lane; p < rs; p += 32) dst[(size_t)i * rs + p] = stg[i * ld + p];
+      flush_rows(stg_a, ld, rs, ka + ((size_t)y * npad + n0) * rs, lane);
+      flush_rows(stg_b, ld, rs, kb + ((size_t)y * npad + n0) * rs, lane);
+    } else {
+      if (job) {
+        for (int p = 0; p < nc; p++) {
+          const float v = w_value<NS>(s_coef[p], h, j);
+          row_a[p] = v;
+          const unsigned uo = ord_float_d(v);
+          lo = uo < lo ? uo : lo;
+          hi = uo > hi ? uo : hi;
+        }
+      } else {
+        for (int p = 0; p < nc; p++) row_a[p] = -1e30f;
+      }
+      for (int p = nc; p < rs; p++) row_a[p] = -1e30f;
       __syncwarp();
+      flush_rows(stg_a, ld, rs, w + ((((size_t)slot * sp.n_states + state) * npad) + n0) * rs, lane);
     }
   }
   if (!is_w) return;
@@ -245,6 +271,7 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
 // n_jobs) gets A = B = kPadMargin (infeasible) and W = 0. Grid (x: blocks of
 // kProjJobs jobs, y: role * n_stages + stage). Values are recomputed from hj
 // with the projection's own functions (bit-identical to ka / kb / w).
+template <int NS>
 __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restrict__ hj,
                                                            const float* __restrict__ coef_c,
                                                            const float* __restrict__ coef_d, const SpaceParams sp,
@@ -255,18 +282,18 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   __shared__ float s_stage[kProjWarps][32 * ld];
   __shared__ float s_lo, s_inv;
   const int role = blockIdx.y / sp.n_stages, stage = blockIdx.y - role * sp.n_stages;
-  const int slot = role / (sp.n_slots + 1), kind = role % (sp.n_slots + 1);  // 0 = A, n_slots = W, else B
-  const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);              // real configs in this stage
+  const int slot = role / (NS + 1), kind = role % (NS + 1);  // 0 = A, NS = W, else B
+  const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);  // real configs in this stage
   if (threadIdx.x == 0) {
     float span = 0.0f;
-    for (int i = 0; i < sp.n_slots; i++) span += unord_float_d(wmm[2 * i + 1]) - unord_float_d(wmm[2 * i]);
+    for (int i = 0; i < NS; i++) span += unord_float_d(wmm[2 * i + 1]) - unord_float_d(wmm[2 * i]);
     s_lo = unord_float_d(wmm[2 * slot]);
-    s_inv = span > 0.0f ? (float)(33554430 - sp.n_slots) / span : 0.0f;
+    s_inv = span > 0.0f ? (float)(33554430 - NS) / span : 0.0f;
   }
   if (threadIdx.x < ncol) {
     const int c = stage * kStageCfg + threadIdx.x, st = c / sp.n_caps, p = c - st * sp.n_caps;
     CoefRow r;
-    if (kind == sp.n_slots) {
+    if (kind == NS) {
       load_w_row(r, sp, coef_c, coef_d, slot, st, p);
     } else if (kind == 0) {
       load_c(r, sp, coef_c, sp.slice[st][slot], p);
@@ -282,39 +309,31 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   const size_t npad = (size_t)sp.n_jobs_pad;
   const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
   if (n0 >= (int64_t)npad) return;
-  const float lo = s_lo, inv = s_inv;
-  float* stg = s_stage[warp];
+  float* row = s_stage[warp] + lane * ld;
   const bool job = n < n_jobs;
   float h[6], j[3];
   if (job) load_hj(hj, n, h, j);
-#pragma unroll 4
-  for (int col = 0; col < kStageCfg; col++) {
-    const bool pad = col >= ncol || !job;
-    float v;
-    if (kind == sp.n_slots) {
-      unsigned bits = 0u;
-      if (!pad) {
-        const float qf = rintf((w_value(sp, s_coef[col], h, j) - lo) * inv);
-        bits = (qf > 0.0f ? (unsigned)qf : 0u) << 5;
-        if (slot == 0) bits += 0x00800000u;
-        if (slot == sp.n_slots - 1) bits |= (unsigned)(31 - col);
-      }
-      v = __uint_as_float(bits);
-    } else if (pad) {
-      v = kPadMargin;
-    } else {
-      v = kind == 0 ? ka_value(sp, s_coef[col], h) : kb_value(s_coef[col], j);
+  const int nreal = job ? ncol : 0;
+  if (kind == NS) {
+    const float lo = s_lo, inv = s_inv;
+    const unsigned base = slot == 0 ? 0x00800000u : 0u;
+    for (int col = 0; col < nreal; col++) {
+      const float qf = rintf((w_value<NS>(s_coef[col], h, j) - lo) * inv);
+      unsigned bits = ((qf > 0.0f ? (unsigned)qf : 0u) << 5) + base;
+      if (slot == NS - 1) bits |= (unsigned)(31 - col);
+      row[col] = __uint_as_float(bits);
     }
-    stg[lane * ld + col] = v;
+    for (int col = nreal; col < kStageCfg; col++) row[col] = 0.0f;
+  } else if (kind == 0) {
+    for (int col = 0; col < nreal; col++) row[col] = ka_value(sp, s_coef[col], h);
+    for (int col = nreal; col < kStageCfg; col++) row[col] = kPadMargin;
+  } else {
+    for (int col = 0; col < nreal; col++) row[col] = kb_value(s_coef[col], j);
+    for (int col = nreal; col < kStageCfg; col++) row[col] = kPadMargin;
   }
   __syncwarp();
-  float* dst = fast + (((size_t)role * sp.n_stages + stage) * npad + n0) * kStageRS;
   static_assert(kStageRS == kStageCfg, "the stage row is exactly the stage's configs");
-#pragma unroll 4
-  for (int k = 0; k < kStageCfg; k++) {
-    const int e = k * 32 + lane, i = e / kStageCfg, c = e - i * kStageCfg;
-    dst[e] = stg[i * ld + c];
-  }
+  flush_rows(s_stage[warp], ld, kStageCfg, fast + (((size_t)role * sp.n_stages + stage) * npad + n0) * kStageRS, lane);
 }
 
 __global__ void k_init_wmm(unsigned* wmm) {
@@ -327,11 +346,25 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   if (n_jobs <= 0) return;
   k_init_wmm<<<1, 32, 0, st>>>(wmm);
   const unsigned jb = (unsigned)((sp.n_jobs_pad + kProjJobs - 1) / kProjJobs);
-  const size_t stage_bytes = (size_t)kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 35 KB (rs <= 68)
-  k_project_all<<<dim3(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states)), kProjJobs, stage_bytes, st>>>(
-      hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
-  k_gather_fast<<<dim3(jb, (unsigned)(sp.n_roles * sp.n_stages)), kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp,
-                                                                                       n_jobs, err, wmm, fast);
+  const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 70 KB (rs <= 68)
+  const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_project_all<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+    cudaFuncSetAttribute(k_project_all<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+    cudaFuncSetAttribute(k_project_all<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+    attr = true;
+  }
+  if (sp.n_slots == 1) {
+    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_gather_fast<1><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+  } else if (sp.n_slots == 2) {
+    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_gather_fast<2><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+  } else {
+    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_gather_fast<3><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -457,11 +490,29 @@ int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const f
 // and reports the winner's RPerf, Throughput, Fairness in natural units
 // (RPerf_i = r_i''/K + alpha).
 // out row (8 floats): [0] cfg (int bits, -1 none), [1] obj, [2] thr, [3] fair, [4..] rperf
+// set_ids == nullptr: one block for the set named by the packed key *key_src
+// (the best set after the all-reduce; key 0 = none -> cfg -1), so best_set
+// needs a single device -> host round trip.
 __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
-                              const float* __restrict__ w, const int64_t* __restrict__ set_ids, float* out_all) {
+                              const float* __restrict__ w, const int64_t* __restrict__ set_ids,
+                              const unsigned long long* __restrict__ key_src, float* out_all) {
   __shared__ unsigned long long s_key[32];
-  const int64_t set_id = set_ids[blockIdx.x];
   float* out = out_all + (int64_t)blockIdx.x * 8;
+  int64_t set_id;
+  if (set_ids) {
+    set_id = set_ids[blockIdx.x];
+  } else {
+    const unsigned long long kk = *key_src;
+    if (kk == 0ull) {
+      if (threadIdx.x == 0) {
+        out[0] = __int_as_float(-1);
+        out[1] = -INFINITY;
+        out[2] = out[3] = 0.0f;
+      }
+      return;
+    }
+    set_id = (int64_t)(0xFFFFFFFFull - (kk & 0xFFFFFFFFull));
+  }
   int64_t j[3];
   if (sp.n_slots == 1) unrank_set<1>(set_id, j);
   else if (sp.n_slots == 2) unrank_set<2>(set_id, j);
@@ -522,7 +573,12 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
 void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
                         int64_t n, float* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, out);
+  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out);
+}
+
+void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
+                        const unsigned long long* key, float* out, cudaStream_t st) {
+  k_sets_detail<<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, out);
 }
 
 // Rank sort of a short list of unique keys, descending: position of key i =
