@@ -169,7 +169,11 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.hist = (unsigned*)take((size_t)kHistBins * 4);
   w.mm = (unsigned*)take(16);
   // nranks = 0: no communicator; else the greedy all-gathers per-rank batches
-  const int64_t cap = nranks > 0 ? std::min<int64_t>(n_sets_local, (int64_t)16 << 20) : n_sets_local;
+  // COSCHED_GREEDY_BATCH_CAP (testing knob): a smaller per-rank batch capacity, which
+  // forces the locally-dominant-rounds fallback of the multi-rank greedy
+  int64_t cap_max = (int64_t)16 << 20;
+  if (const char* e = getenv("COSCHED_GREEDY_BATCH_CAP")) cap_max = std::max<int64_t>(1, atoll(e));
+  const int64_t cap = nranks > 0 ? std::min<int64_t>(n_sets_local, cap_max) : n_sets_local;
   w.batch_cap = cap;
   const int64_t gathered = nranks > 0 ? cap * nranks : 0;
   w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);

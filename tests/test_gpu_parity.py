@@ -348,3 +348,21 @@ def test_one_rank_nccl_communicator_matches_no_comm(cs):
     for s in (a, b):
         s.score_all(torch.from_numpy(F).cuda())
     assert a.best_allocation(20) == b.best_allocation(20)
+
+
+@pytest.mark.parametrize("table,n,k", [("b200", 300, 150), ("b200_3way", 45, 15)])
+def test_greedy_fallback_rounds_match_sorted_scan(cs, table, n, k, monkeypatch):
+    """With a communicator, a batch larger than the per-rank capacity switches the greedy to
+    the locally-dominant-rounds fallback; forcing it (COSCHED_GREEDY_BATCH_CAP) must give the
+    same picks as the sorted scan (both are the exact sequential greedy)."""
+    pb = make_problem(table, "c10", coef_seed=121, alpha=0.2)
+    F, _ = make_features(n, seed=122)
+    a = cs.Scheduler(pb)
+    a.score_all(torch.from_numpy(F).cuda())
+    ref = a.best_allocation(k)
+    monkeypatch.setenv("COSCHED_GREEDY_BATCH_CAP", "64")
+    b = cs.Scheduler(pb)
+    b.set_comm(cs.get_unique_id(), 0, 1)
+    b.score_all(torch.from_numpy(F).cuda())
+    got = b.best_allocation(k)
+    assert b.greedy_rounds > 1 and got == ref
