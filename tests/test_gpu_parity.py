@@ -366,3 +366,36 @@ def test_greedy_fallback_rounds_match_sorted_scan(cs, table, n, k, monkeypatch):
     b.score_all(torch.from_numpy(F).cuda())
     got = b.best_allocation(k)
     assert b.greedy_rounds > 1 and got == ref
+
+
+@pytest.mark.parametrize("W", [3, 8])
+@pytest.mark.parametrize("table", ["b200", "b200_3way"])
+def test_fake_ranks_hill_truth_and_triples(cs, W, table):
+    """Sharded by W fake ranks, the hill-climbing outputs and the triple scorer's outputs are
+    bit-identical to one rank, and the ground-truth summary sums over the shards."""
+    from synth.ground_truth import B200
+    pb = make_problem(table, "c10", coef_seed=16, alpha=0.25)
+    F, _ = make_features(120 if table == "b200" else 40, seed=16)
+    Fd = torch.from_numpy(F).cuda()
+    for mode in (0, 1):
+        ref = cs.Scheduler(pb)
+        ref.set_search(mode, 2, 3)
+        o1, c1 = ref.score_all(Fd)
+        o1, c1 = o1.cpu().numpy(), c1.cpu().numpy()
+        _, sm1 = ref.evaluate_truth(Fd, B200)
+        objs, cfgs, n_cmp, n_vio, lsum = [], [], 0, 0, 0.0
+        for r in range(W):
+            s = cs.Scheduler(pb)
+            s.set_search(mode, 2, 3)
+            s.set_shard_view(r, W)
+            o, c = s.score_all(Fd)
+            objs.append(o.cpu().numpy())
+            cfgs.append(c.cpu().numpy())
+            _, sm = s.evaluate_truth(Fd, B200)
+            n_cmp += sm["n_compared"]
+            n_vio += sm["n_violations"]
+            if sm["n_compared"]:
+                lsum += sm["n_compared"] * math.log(sm["geomean_prop_over_best"])
+        assert np.array_equal(np.concatenate(cfgs), c1) and np.array_equal(np.concatenate(objs), o1)
+        assert n_cmp == sm1["n_compared"] and n_vio == sm1["n_violations"]
+        assert abs(math.exp(lsum / n_cmp) - sm1["geomean_prop_over_best"]) <= 1e-9
