@@ -94,14 +94,19 @@ __device__ __forceinline__ void issue_tstage(float* stage, uint64_t* bar, const 
 // Partner partials of a landed stage, in place over its j1 blocks:
 // P1 -> [4], P0 -> [5], P2 -> [6], Q -> [7] (canonical order of eval_cfg<3>).
 __device__ __forceinline__ void tstage_partials(float* st) {
-  constexpr int rs = kStageRS, blk = kTT * kStageRS;
-  const float* rows = st + 8 * blk;
-  for (int e = threadIdx.x; e < blk; e += kTThreads) {
-    const int c = e % rs;
-    st[4 * blk + e] = __fadd_rn(st[4 * blk + e], rows[2 * rs + c]);  // P1 = ka[s1][j1] + kb[s1][j2]
-    st[5 * blk + e] = __fadd_rn(st[5 * blk + e], rows[1 * rs + c]);  // P0 = kb[s0][j1] + kb[s0][j2]
-    st[6 * blk + e] = __fadd_rn(rows[0 * rs + c], st[6 * blk + e]);  // P2 = ka[s2][j2] + kb[s2][j1]
-    st[7 * blk + e] = __uint_as_float(__float_as_uint(st[7 * blk + e]) + __float_as_uint(rows[3 * rs + c]));
+  constexpr int rs4 = kStageRS / 4, blk4 = kTT * rs4;  // float4 per role block
+  float4* s4 = reinterpret_cast<float4*>(st);
+  const float4* rows = s4 + 8 * blk4;  // the 4 single j2 rows (rs4 float4 each)
+  for (int e = threadIdx.x; e < blk4; e += kTThreads) {
+    const int c = e % rs4;
+    const float4 r0 = rows[c], r1 = rows[rs4 + c], r2 = rows[2 * rs4 + c], r3 = rows[3 * rs4 + c];
+    s4[4 * blk4 + e] = add4(s4[4 * blk4 + e], r2);  // P1 = ka[s1][j1] + kb[s1][j2]
+    s4[5 * blk4 + e] = add4(s4[5 * blk4 + e], r1);  // P0 = kb[s0][j1] + kb[s0][j2]
+    s4[6 * blk4 + e] = add4(r0, s4[6 * blk4 + e]);  // P2 = ka[s2][j2] + kb[s2][j1]
+    const uint4 q = reinterpret_cast<const uint4*>(s4)[7 * blk4 + e];
+    const uint4 w2 = make_uint4(__float_as_uint(r3.x), __float_as_uint(r3.y), __float_as_uint(r3.z),
+                                __float_as_uint(r3.w));
+    reinterpret_cast<uint4*>(s4)[7 * blk4 + e] = make_uint4(q.x + w2.x, q.y + w2.y, q.z + w2.z, q.w + w2.w);  // Q
   }
 }
 
