@@ -283,6 +283,7 @@ def calibration_metrics(pb, F, dev, args):
     sf = cs.Scheduler(pbf, device=dev.index or 0)
     Fd = targs[0]
     sf.score_all(Fd)
+    sf.evaluate_truth(Fd, truth)  # warm: output buffers, lazy module load
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     _, summ = sf.evaluate_truth(Fd, truth)

@@ -37,6 +37,7 @@ struct TruthParams {
   int8_t gpcs[kMaxStates][kMaxSlots];
   int8_t mem[kMaxStates];
   float caps[kMaxCaps];
+  float inv_caps[kMaxCaps];
 };
 
 __device__ __forceinline__ float raw_rperf(const TruthParams& q, const float* c, const float* b, const float* t,
@@ -93,20 +94,45 @@ __global__ void __launch_bounds__(256) k_truth_sets(const TruthParams q, const f
     }
     const int pc = prop_cfg[k];
     float best = -INFINITY, worst = INFINITY, po = -INFINITY, pf = -INFINITY;
-    for (int s = 0; s < q.n_states; s++) {
-      int g[NS];
+    // hoisted per set: c_eff, the sum of bandwidth demands, reciprocals
+    float ceff[NS], inv_c[NS], inv_b[NS], inv_base[NS], bsum = 0.0f;
 #pragma unroll
-      for (int i = 0; i < NS; i++) g[i] = q.gpcs[s][i];
+    for (int i = 0; i < NS; i++) {
+      ceff[i] = c[i] * (1.0f + q.kappa * t[i]);
+      inv_c[i] = 1.0f / c[i];
+      inv_b[i] = b[i] > 0.0f ? 1.0f / b[i] : 0.0f;
+      inv_base[i] = 1.0f / base[i];
+      bsum += b[i];
+    }
+    for (int s = 0; s < q.n_states; s++) {
+      // per state: the power draw and, per slot, the compute scale and the
+      // memory-bound ceiling (independent of the cap)
+      float draw = q.w_base, kc[NS], rcap[NS];
+#pragma unroll
+      for (int i = 0; i < NS; i++) draw = __fmaf_rn(q.w_gpc * (float)q.gpcs[s][i], ceff[i], draw);
+      const float inv_ded = 1.0f / fmaxf(draw - q.w_base, 1e-12f);
+#pragma unroll
+      for (int i = 0; i < NS; i++) {
+        const int g = q.gpcs[s][i];
+        kc[i] = ((float)g / q.g_full) * inv_c[i];
+        float cap = 1.0f;
+        if (b[i] > 0.0f) {
+          const float memv = q.mem[s] ? q.modules[g] / q.n_modules : (bsum <= 1.0f ? b[i] : b[i] / fmaxf(bsum, 1e-12f));
+          cap = fminf(cap, memv * inv_b[i]);
+        }
+        rcap[i] = cap;
+      }
       for (int p = 0; p < q.n_caps; p++) {
         const float P = q.caps[p];
-        float thr = 0.0f, fair = INFINITY;
+        const float thr = draw > P ? fminf(fmaxf((P - q.w_base) * inv_ded, q.f_min), 1.0f) : 1.0f;
+        float sum = 0.0f, fair = INFINITY;
 #pragma unroll
         for (int i = 0; i < NS; i++) {
-          const float r = raw_rperf(q, c, b, t, g, NS, q.mem[s], P, i) / base[i];
-          thr += r;
+          const float r = fminf(rcap[i], kc[i] * thr) * inv_base[i];
+          sum += r;
           fair = fminf(fair, r);
         }
-        const float o = q.objective == 2 ? thr / P : thr;
+        const float o = q.objective == 2 ? sum * q.inv_caps[p] : sum;
         if (fair > q.alpha) {
           best = fmaxf(best, o);
           worst = fminf(worst, o);
@@ -185,7 +211,10 @@ int truth_enqueue(const cosched_truth_desc* d, const SpaceParams& sp, int object
     for (int i = 0; i < sp.n_slots; i++) q.gpcs[s][i] = (int8_t)gpcs[s * sp.n_slots + i];
     q.mem[s] = (int8_t)mem[s];
   }
-  for (int p = 0; p < sp.n_caps; p++) q.caps[p] = caps[p];
+  for (int p = 0; p < sp.n_caps; p++) {
+    q.caps[p] = caps[p];
+    q.inv_caps[p] = 1.0f / caps[p];
+  }
   char* base = (char*)workspace;
   float4* jp = (float4*)base;
   double* part = (double*)(base + ((size_t)n_jobs * 16 + 255) / 256 * 256);
