@@ -310,6 +310,7 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
   sp.np = (d->n_caps + 3) & ~3;
   sp.rs = ((sp.np >> 2) & 1) ? sp.np : sp.np + 4;
   sp.n_jobs_pad = 0;
+  sp.inv_ncaps = 1.0f / (float)d->n_caps;
   sp.search_mode = 0;  // exhaustive
   sp.hc_state = sp.hc_cap = 0;
 

@@ -53,6 +53,7 @@ struct SpaceParams {
   float alpha;
   int32_t search_mode;        // 0 exhaustive, 1 hill climbing from (hc_state, hc_cap) (R22)
   int32_t hc_state, hc_cap;
+  float inv_ncaps;            // 1 / n_caps (FP32 division-free config decode in the tile ends)
   float inv_p[kMaxCaps];      // per cap: fl(1/P) (Problem 2) or 1 (Problem 1)
   int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
 };

@@ -212,6 +212,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
       // are the stage offset of the argmax, and the reported objective is the
       // exact FP32 w0 + w1 of that config (2 loads).
       constexpr int kPass = 4;
+      const int jI = (int)(I * kTile), jJ = (int)(J * kTile);
+      const int c_lo = (int)g.c0, c_hi = (int)g.c1;  // this shard's columns (c1 <= n_jobs)
+      const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
 #pragma unroll 1
       for (int e0 = 0; e0 < kTile * kTile; e0 += kPass * kThreads) {
         float f0[kPass], f1[kPass];
@@ -220,18 +223,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int u = 0; u < kPass; u++) {
           const int e = e0 + u * kThreads + threadIdx.x;
           const int rj = e >> 6, ri = e & 63;
-          const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+          const int j0 = jI + ri, j1 = jJ + rj;
           const int sg = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
           const unsigned kbits = __float_as_uint(sbest[rj * kBgRow + ri]);
           sbg[rj * kBgRow + ri] = -1;
-          const bool ok = j0 < j1 && j1 < g.n_jobs && j1 >= g.c0 && j1 < g.c1;
+          const bool ok = j0 < j1 && j1 >= c_lo && j1 < c_hi;
           const int c = sg * kStageCfg + 31 - (int)(kbits & 31u);
           c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
           f0[u] = f1[u] = 0.0f;
           if (c_[u] >= 0) {
-            const int st = c / sp.n_caps, p = c - st * sp.n_caps;
-            f0[u] = __ldg(w_row(w, sp, 0, st, j0) + p);
-            f1[u] = __ldg(w_row(w, sp, 1, st, j1) + p);
+            // c / n_caps in FP32: (c + 0.5) / n_caps stays >= 1/128 away from an
+            // integer for c < 2^13, n_caps <= 64, so the truncation is exact
+            const int st = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st * sp.n_caps;
+            const int r0 = st * npad + j0, r1 = w1base + st * npad + j1;  // w rows, < 2^31
+            f0[u] = __ldg(w + (int64_t)r0 * rsz + p);
+            f1[u] = __ldg(w + (int64_t)r1 * rsz + p);
           }
         }
 #pragma unroll
@@ -239,10 +245,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (c_[u] == -2) continue;
           const int e = e0 + u * kThreads + threadIdx.x;
           const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0 of one column
-          const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+          const int j0 = jI + ri, j1 = jJ + rj;
           const int bc = c_[u];
           const float bo = bc >= 0 ? __fadd_rn(f0[u], f1[u]) : -INFINITY;
-          const int64_t sid = j1 * (j1 - 1) / 2 + j0;
+          const int64_t sid = (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
           const int64_t k = sid - g.first_set;
           if (out_obj) out_obj[k] = bo;
           if (out_cfg) out_cfg[k] = bc;

@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(kTThreads, MINB)
           c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
           f0[u] = f1[u] = f2[u] = 0.0f;
           if (c_[u] >= 0) {
-            const int st_ = c / sp.n_caps, p = c - st_ * sp.n_caps;
+            // exact FP32 decode of c / n_caps (see score_pairs.cu)
+            const int st_ = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st_ * sp.n_caps;
             f0[u] = __ldg(w_row(w, sp, 0, st_, j0) + p);
             f1[u] = __ldg(w_row(w, sp, 1, st_, j1) + p);
             f2[u] = __ldg(w_row(w, sp, 2, st_, j2) + p);
