@@ -247,6 +247,10 @@ __global__ void __launch_bounds__(kTThreads, MINB)
       // the argmax config; its exact FP32 objective in the canonical order
       // w0 + (w1 + w2)
       constexpr int kPass = 4;
+      const int jA = (int)(A * kTT), jB = (int)(B * kTT), j2 = (int)J2;
+      const bool plane_ok = J2 < g.n_jobs && J2 >= g.c0 && J2 < g.c1;  // uniform per tile
+      const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, sl = sp.n_states * npad;
+      const int64_t sid2 = (int64_t)j2 * (j2 - 1) * (j2 - 2) / 6;  // colex offset of the plane
 #pragma unroll 1
       for (int e0 = 0; e0 < kTT * kTT; e0 += kPass * kTThreads) {
         float f0[kPass], f1[kPass], f2[kPass];
@@ -255,20 +259,21 @@ __global__ void __launch_bounds__(kTThreads, MINB)
         for (int u = 0; u < kPass; u++) {
           const int e = e0 + u * kTThreads + threadIdx.x;
           const int rj = e >> 6, ri = e & 63;
-          const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
+          const int j0 = jA + ri, j1 = jB + rj;
           const int sg = sbg[rj * kTBgRow + ri];
           const unsigned kbits = __float_as_uint(sbest[rj * kTBgRow + ri]);
           sbg[rj * kTBgRow + ri] = -1;  // every slot, valid or not
-          const bool ok = j0 < j1 && j1 < j2 && j2 < g.n_jobs && j2 >= g.c0 && j2 < g.c1;
+          const bool ok = plane_ok && j0 < j1 && j1 < j2;
           const int c = sg * kStageCfg + (31 - (int)(kbits & 31u));
           c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
           f0[u] = f1[u] = f2[u] = 0.0f;
           if (c_[u] >= 0) {
-            // exact FP32 decode of c / n_caps (see score_pairs.cu)
+            // exact FP32 decode of c / n_caps (see score_pairs.cu); w rows < 2^31
             const int st_ = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st_ * sp.n_caps;
-            f0[u] = __ldg(w_row(w, sp, 0, st_, j0) + p);
-            f1[u] = __ldg(w_row(w, sp, 1, st_, j1) + p);
-            f2[u] = __ldg(w_row(w, sp, 2, st_, j2) + p);
+            const int r = st_ * npad;
+            f0[u] = __ldg(w + (int64_t)(r + j0) * rsz + p);
+            f1[u] = __ldg(w + (int64_t)(sl + r + j1) * rsz + p);
+            f2[u] = __ldg(w + (int64_t)(2 * sl + r + j2) * rsz + p);
           }
         }
 #pragma unroll
@@ -276,10 +281,10 @@ __global__ void __launch_bounds__(kTThreads, MINB)
           if (c_[u] == -2) continue;
           const int e = e0 + u * kTThreads + threadIdx.x;
           const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0
-          const int64_t j0 = A * kTT + ri, j1 = B * kTT + rj, j2 = J2;
+          const int j0 = jA + ri, j1 = jB + rj;
           const int bc = c_[u];
           const float bo = bc >= 0 ? __fadd_rn(f0[u], __fadd_rn(f1[u], f2[u])) : -INFINITY;
-          const int64_t sid = j2 * (j2 - 1) * (j2 - 2) / 6 + j1 * (j1 - 1) / 2 + j0;
+          const int64_t sid = sid2 + (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
           const int64_t k = sid - g.first_set;
           if (out_obj) out_obj[k] = bo;
           if (out_cfg) out_cfg[k] = bc;
