@@ -773,7 +773,12 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   // 2. batches of bins, from the top, of ~kBatch keys (global)
   // a batch is a range of objective bins holding ~kBatch feasible sets; only the
   // sets whose jobs are all still free are compacted and sorted
-  const int64_t kBatch = std::min<int64_t>(ws.batch_cap, (int64_t)64 << 20);
+  // batch sizes grow geometrically from 8 M keys (a first batch that already holds
+  // the k picks sorts little; deep scans reach 64 M keys per batch after 3 rounds)
+  int64_t batch_keys = (int64_t)64 << 20, batch_first = (int64_t)8 << 20;
+  if (const char* e = getenv("COSCHED_GREEDY_BATCH")) batch_keys = batch_first = std::max<int64_t>(1024, atoll(e));
+  const int64_t kBatchMax = std::min<int64_t>(ws.batch_cap, batch_keys);
+  int64_t kBatch = std::min<int64_t>(kBatchMax, batch_first);
   uint32_t* taken_bits = ws.taken;
   CK(cudaMemsetAsync(taken_bits, 0, (size_t)((N + 31) / 32) * 4, s));
   int64_t* np_dev = ws.counters + 1;
@@ -795,7 +800,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     // (sets of earlier batches were picked or blocked, so no bin filter is needed)
     const int64_t n_free = N - (int64_t)ns * n_picks;
     const int64_t n_comb = cosched::n_sets(n_free, ns);
-    endgame = n_picks > 0 && n_comb <= kBatch && n_comb * 8 <= cosched::n_sets(N, ns);  // gathers << a full scan
+    endgame = n_picks > 0 && n_comb <= kBatchMax && n_comb * 8 <= cosched::n_sets(N, ns);  // gathers << a full scan
     // 3. compact this rank's keys in the range (or of the free jobs); gather over ranks; sort; scan
     CK(cudaMemsetAsync(nk_dev, 0, 8, s));
     if (endgame) {
@@ -856,6 +861,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       CK(cudaStreamSynchronize(s));
     }
     bin_hi = bin_lo - 1;
+    kBatch = std::min<int64_t>(kBatchMax, kBatch * 2);
   }
   picks->resize(n_picks);
   if (n_picks) {
