@@ -1173,6 +1173,8 @@ cosched_status cosched_evaluate_truth(cosched_t h, const cosched_truth_desc* tru
     return fail(h, COSCHED_E_OOM, "workspace too small");
   (void)n_rows;
   DeviceGuard g(h->device);
+  cosched_status vs = check_deferred(h);  // the scored features were valid
+  if (vs != COSCHED_OK) return vs;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   int n = truth_enqueue(truth, h->sp, h->objective, h->h_gpcs.data(), h->h_mem.data(), h->h_caps.data(), features_dev,
                         jobs_dev, h->n_jobs, h->first, h->n_sets, h->out_cfg, out, workspace, h->d_sums, st);
