@@ -339,6 +339,44 @@ def hill_metrics(sched, Fd, pb, stream, args):
     return out
 
 
+def shard_projection(sched, Fd, stream, t1_ms, cand_per_step, args):
+    """Strong-scaling projection on ONE GPU: every rank's shard of a W-way run
+    (cosched_set_shard_view, the same set ranges cosched_shard_range gives rank r
+    of W) timed alone as a full step (validate + project + gather + score + local
+    best), L2 flushed between steps. The W-GPU step is bounded below by the
+    slowest shard; the NCCL u64 max all-reduce (~10-30 us over NVLink, SURVEY
+    8(e)) is not included. A projection, not a multi-GPU measurement."""
+    import torch
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=Fd.device)
+    out = {"method": "each rank's shard timed alone on one GPU (fake-rank view), max over ranks; "
+                     "excludes the NCCL all-reduce", "t1_ms": t1_ms, "per_w": {}}
+    for W in args.shard_ws:
+        per_rank = []
+        for r in range(W):
+            sched.set_shard_view(r, W)
+            for _ in range(2):
+                sched.score_all(Fd, None, with_out=True, stream=stream)
+                sched.best_set()
+            ts = []
+            for k in range(args.shard_steps):
+                flush.fill_(k & 0xFF)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                sched.score_all(Fd, None, with_out=True, stream=stream)
+                sched.best_set()
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            per_rank.append(statistics.median(ts))
+        sched.set_shard_view(0, 1)
+        tmax = max(per_rank)
+        out["per_w"][str(W)] = {"max_ms": tmax, "min_ms": min(per_rank), "per_rank_ms": per_rank,
+                                "projected_speedup": t1_ms / tmax,
+                                "projected_candidates_per_s": cand_per_step / (tmax * 1e-3)}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -499,6 +537,8 @@ def run_ours(args):
             "node_budget": node_info,
             "clocks": clocks,
         }
+        if args.shard_ws and world == 1:
+            line["shard_projection"] = shard_projection(sched, Fd, stream, ms_per_step, cand_per_step, args)
         if args.hill:
             line["hill_climb"] = hill_metrics(sched, Fd, pb, stream, args)
         if args.calib_coruns > 0:
@@ -525,6 +565,9 @@ def main():
     ap.add_argument("--calib-coruns", type=int, default=1000000,
                     help="co-runs of the calibration timing (0: skip the calibration measurement)")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--shard-ws", type=lambda s: [int(x) for x in s.split(",") if x], default=[2, 4, 8],
+                    help="W values of the one-GPU strong-scaling projection (empty: skip)")
+    ap.add_argument("--shard-steps", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -132,8 +132,11 @@ cosched_status cosched_set_comm(cosched_t h, const void* nccl_unique_id, int ran
 cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks);
 
 /* This rank's set range for a queue of n_jobs (host only, no CUDA). Rank r of
- * W gets the sets whose largest position lies in [b_r, b_{r+1}), with b_r
- * the smallest b such that C(b, n_slots) >= r * C(n_jobs, n_slots) / W. */
+ * W gets the sets whose largest position lies in [b_r, b_{r+1}). Pairs (and
+ * solo): b_r is the smallest b with C(b, n_slots) >= r * C(n_jobs, n_slots) / W
+ * (balanced on sets). Triples: balanced on the triple scorer's work instead,
+ * b_r the smallest b with T(b) >= r * T(n_jobs) / W, where T(b) = sum over
+ * planes 1 <= j < b of t(t+1)/2 with t = ceil(j / 64) (its 64 x 64 tiles). */
 cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets);
 
 /* The same partition without a handle (host only): rank of nranks, sets of n_slots jobs. */

@@ -446,9 +446,17 @@ void cosched_unpack_key(uint64_t key, float* obj, int64_t* set_id) {
   if (set_id) *set_id = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
 }
 
+// Contiguous whole-column shards. Pairs: balanced on sets, b_r the smallest b
+// with C(b,2) >= ceil(r * total / W). Triples: balanced on the triple scorer's
+// tiles (its time per plane follows the tile count, the small planes' diagonal
+// and ragged tiles included), b_r the smallest b with tiles_before(b) >=
+// ceil(r * tiles_before(n_jobs) / W).
 static void shard_bounds(int64_t n_jobs, int k, int rank, int nranks, int64_t* first, int64_t* count) {
-  int64_t total = cosched::n_sets(n_jobs, k);
-  auto boundary = [&](int r) -> int64_t {  // smallest b with C(b,k) >= ceil(r * total / W)
+  auto cost = [&](int64_t b) -> int64_t {
+    return k == 3 ? cosched::triple_tiles_before(b) : cosched::n_sets(b, k);
+  };
+  const int64_t total = cost(n_jobs);
+  auto boundary = [&](int r) -> int64_t {  // smallest b with cost(b) >= ceil(r * total / W)
     if (r <= 0) return 0;
     if (r >= nranks) return n_jobs;
     __int128 num = (__int128)r * total;
@@ -456,7 +464,7 @@ static void shard_bounds(int64_t n_jobs, int k, int rank, int nranks, int64_t* f
     int64_t lo = 0, hi = n_jobs;
     while (lo < hi) {
       int64_t mid = (lo + hi) / 2;
-      if (cosched::n_sets(mid, k) >= target) hi = mid;
+      if (cost(mid) >= target) hi = mid;
       else lo = mid + 1;
     }
     return lo;

@@ -183,6 +183,9 @@ void launch_fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t st);
 
 // host-side helpers shared by the API (no CUDA)
 int64_t n_sets(int64_t n, int k);
+// tiles of the triple scorer's planes j2' < j2 (score_triples.cu): the work
+// measure the triple shards are balanced on
+int64_t triple_tiles_before(int64_t j2);
 uint32_t ord_float(float f);
 float unord_float(uint32_t o);
 

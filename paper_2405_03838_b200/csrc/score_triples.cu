@@ -110,6 +110,73 @@ __device__ __forceinline__ void tstage_partials(float* st) {
   }
 }
 
+// One stage of a tile: every (j0, j1) entry of the thread's 4 x 4 micro-tile
+// (j0 = 64 A + tx + 16 a, j1 = 64 B + ty + 16 b) against the stage's configs.
+// DIAG skips the entries a > b; only the row groups b < NBV are evaluated.
+template <bool DIAG, int NBV>
+__device__ __forceinline__ void tstage_body(const float* st, int tx, int ty, unsigned one, int s,
+                                            float (&breg)[kTM][kTM], int16_t* sbg) {
+  constexpr int rs4 = kStageRS / 4, chunks = kStageCfg / 4;
+  const float4* st4 = reinterpret_cast<const float4*>(st);
+  constexpr int blk4 = kTT * rs4;
+  const float4* A0 = st4 + 0 * blk4 + tx * rs4;
+  const float4* B01 = st4 + 1 * blk4 + tx * rs4;
+  const float4* B02 = st4 + 2 * blk4 + tx * rs4;
+  const uint4* W0 = reinterpret_cast<const uint4*>(st4 + 3 * blk4 + tx * rs4);
+  const float4* P1 = st4 + 4 * blk4 + ty * rs4;
+  const float4* P0 = st4 + 5 * blk4 + ty * rs4;
+  const float4* P2 = st4 + 6 * blk4 + ty * rs4;
+  const uint4* Q = reinterpret_cast<const uint4*>(st4 + 7 * blk4 + ty * rs4);
+  constexpr int row16 = 16 * rs4;
+
+  float m[kTM][kTM];
+#pragma unroll
+  for (int q = 0; q < chunks; q++) {
+    float4 p0[NBV], p1[NBV], p2[NBV];
+    uint4 qv[NBV];
+#pragma unroll
+    for (int b = 0; b < NBV; b++) {
+      p0[b] = P0[b * row16 + q];
+      p1[b] = P1[b * row16 + q];
+      p2[b] = P2[b * row16 + q];
+      qv[b] = Q[b * row16 + q];
+    }
+#pragma unroll
+    for (int a = 0; a < kTM; a++) {
+      if (DIAG && a >= NBV) continue;  // a > b for every evaluated b
+      const float4 a0 = A0[a * row16 + q];
+      const float4 b01 = B01[a * row16 + q];
+      const float4 b02 = B02[a * row16 + q];
+      const uint4 w0 = W0[a * row16 + q];
+#pragma unroll
+      for (int b = 0; b < NBV; b++) {
+        if (DIAG && a > b) continue;
+        const float4 r0 = add4(a0, p0[b]);
+        const float4 r1 = add4(p1[b], b01);
+        const float4 r2 = add4(p2[b], b02);
+        const float x0 = min3f(__uint_as_float(imad_add(w0.x, one, qv[b].x)), r0.x, fminf(r1.x, r2.x));
+        const float x1 = min3f(__uint_as_float(imad_add(w0.y, one, qv[b].y)), r0.y, fminf(r1.y, r2.y));
+        const float x2 = min3f(__uint_as_float(imad_add(w0.z, one, qv[b].z)), r0.z, fminf(r1.z, r2.z));
+        const float x3 = min3f(__uint_as_float(imad_add(w0.w, one, qv[b].w)), r0.w, fminf(r1.w, r2.w));
+        if (q == 0)
+          m[a][b] = fmaxf(max3f(x0, x1, x2), x3);
+        else
+          m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < kTM; a++)
+#pragma unroll
+    for (int b = 0; b < NBV; b++) {
+      if (DIAG && a > b) continue;
+      if (m[a][b] > breg[a][b]) {
+        breg[a][b] = m[a][b];
+        sbg[(ty + 16 * b) * kTBgRow + tx + 16 * a] = (int16_t)s;
+      }
+    }
+}
+
 }  // namespace
 
 template <int MINB>
@@ -178,60 +245,23 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 
     float* st = smem + buf * stage_floats;  // landed, partials built (previous iteration)
 
-    const float4* st4 = reinterpret_cast<const float4*>(st);
-    constexpr int blk4 = kTT * rs4;
-    const float4* A0 = st4 + 0 * blk4 + tx * rs4;
-    const float4* B01 = st4 + 1 * blk4 + tx * rs4;
-    const float4* B02 = st4 + 2 * blk4 + tx * rs4;
-    const uint4* W0 = reinterpret_cast<const uint4*>(st4 + 3 * blk4 + tx * rs4);
-    const float4* P1 = st4 + 4 * blk4 + ty * rs4;
-    const float4* P0 = st4 + 5 * blk4 + ty * rs4;
-    const float4* P2 = st4 + 6 * blk4 + ty * rs4;
-    const uint4* Q = reinterpret_cast<const uint4*>(st4 + 7 * blk4 + ty * rs4);
-    constexpr int row16 = 16 * rs4;
-
-    float m[kTM][kTM];
-#pragma unroll
-    for (int q = 0; q < chunks; q++) {
-      float4 p0[kTM], p1[kTM], p2[kTM];
-      uint4 qv[kTM];
-#pragma unroll
-      for (int b = 0; b < kTM; b++) {
-        p0[b] = P0[b * row16 + q];
-        p1[b] = P1[b * row16 + q];
-        p2[b] = P2[b * row16 + q];
-        qv[b] = Q[b * row16 + q];
-      }
-#pragma unroll
-      for (int a = 0; a < kTM; a++) {
-        const float4 a0 = A0[a * row16 + q];
-        const float4 b01 = B01[a * row16 + q];
-        const float4 b02 = B02[a * row16 + q];
-        const uint4 w0 = W0[a * row16 + q];
-#pragma unroll
-        for (int b = 0; b < kTM; b++) {
-          const float4 r0 = add4(a0, p0[b]);
-          const float4 r1 = add4(p1[b], b01);
-          const float4 r2 = add4(p2[b], b02);
-          const float x0 = min3f(__uint_as_float(imad_add(w0.x, one, qv[b].x)), r0.x, fminf(r1.x, r2.x));
-          const float x1 = min3f(__uint_as_float(imad_add(w0.y, one, qv[b].y)), r0.y, fminf(r1.y, r2.y));
-          const float x2 = min3f(__uint_as_float(imad_add(w0.z, one, qv[b].z)), r0.z, fminf(r1.z, r2.z));
-          const float x3 = min3f(__uint_as_float(imad_add(w0.w, one, qv[b].w)), r0.w, fminf(r1.w, r2.w));
-          if (q == 0)
-            m[a][b] = fmaxf(max3f(x0, x1, x2), x3);
-          else
-            m[a][b] = max3f(max3f(m[a][b], x0, x1), x2, x3);
-        }
-      }
+    // tile shape (uniform per block): on the diagonal (a == b) the micro-tile
+    // entries a > b are never valid (j0 - j1 >= 1) and are skipped; in the last
+    // j1 block of the plane only the first ceil((j2 - 64 b) / 16) row groups hold
+    // j1 < j2
+    const int nbv_raw = (int)((J2 - B * kTT + 15) >> 4);
+    const int nbv = nbv_raw > kTM ? kTM : (nbv_raw < 1 ? 1 : nbv_raw);
+    const int shape = (A == B ? 4 : 0) + nbv - 1;
+    switch (shape) {
+      case 0: tstage_body<false, 1>(st, tx, ty, one, s, breg, sbg); break;
+      case 1: tstage_body<false, 2>(st, tx, ty, one, s, breg, sbg); break;
+      case 2: tstage_body<false, 3>(st, tx, ty, one, s, breg, sbg); break;
+      case 3: tstage_body<false, 4>(st, tx, ty, one, s, breg, sbg); break;
+      case 4: tstage_body<true, 1>(st, tx, ty, one, s, breg, sbg); break;
+      case 5: tstage_body<true, 2>(st, tx, ty, one, s, breg, sbg); break;
+      case 6: tstage_body<true, 3>(st, tx, ty, one, s, breg, sbg); break;
+      default: tstage_body<true, 4>(st, tx, ty, one, s, breg, sbg); break;
     }
-#pragma unroll
-    for (int a = 0; a < kTM; a++)
-#pragma unroll
-      for (int b = 0; b < kTM; b++)
-        if (m[a][b] > breg[a][b]) {
-          breg[a][b] = m[a][b];
-          sbg[(ty + 16 * b) * kTBgRow + tx + 16 * a] = (int16_t)s;
-        }
 
     if (s == sp.n_stages - 1) {
 #pragma unroll
@@ -313,6 +343,9 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   }
   block_max_key(key, best_key);
 }
+
+// Host view of the tile count, for work-balanced triple shards (api.cu shard_bounds).
+int64_t triple_tiles_before(int64_t j2) { return tiles_before(j2); }
 
 static int g_tri_sms = 0;
 

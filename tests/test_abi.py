@@ -79,8 +79,18 @@ def test_shards_partition_whole_columns(cs, n, k):
                 cols = [c for c in range(n + 1) if math.comb(c, k) == a]
                 assert cols
         assert nxt == total
-        if total >= 1000 * W:
+        if total >= 1000 * W and k == 2:
             assert max(sizes) - min(sizes) <= 2 * max(math.comb(n - 1, k - 1), 1)  # one column each side
+        if total >= 1000 * W and k == 3:
+            # triples balance the scorer's 64 x 64 tiles per plane (cosched.h): per-rank
+            # tile counts within one plane's tiles of each other
+            def plane_tiles(j):
+                t = -(-j // 64)
+                return t * (t + 1) // 2
+            cols = [next(c for c in range(n + 1) if math.comb(c, 3) >= a) for a in
+                    [sum(sizes[:r]) for r in range(W)]] + [n]
+            tiles = [sum(plane_tiles(j) for j in range(max(cols[r], 1), cols[r + 1])) for r in range(W)]
+            assert max(tiles) - min(tiles) <= 2 * plane_tiles(n - 1)
 
 
 def test_compute_fails_loudly_without_gpu(cs):
