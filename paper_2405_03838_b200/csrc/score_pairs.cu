@@ -50,6 +50,8 @@ struct PairGrid {
   int64_t n_tiles;
   int64_t base;       // tiles before the first column tile: jt0*(jt0+1)/2
   int64_t first_set;  // output index offset
+  int64_t t0;         // first tile of this launch
+  int64_t n_units;    // work units of this launch: a unit is a tile's j1 row groups [b0, b0 + NB)
   unsigned one;       // runtime 1: keeps the integer adds on the FMA pipe (IMAD)
 };
 
@@ -61,6 +63,15 @@ __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_
   while ((j + 1) * (j + 2) / 2 <= u) j++;
   *J = j;
   *I = u - j * (j + 1) / 2;
+}
+
+// Work unit u of a launch with NB row groups (of 16 j1 rows) per unit -> tile
+// (I, J) and its first row group b0. NB = 4: whole tiles.
+template <int NB>
+__device__ __forceinline__ void unit_coords(const PairGrid& g, int64_t u, int64_t* I, int64_t* J, int* b0) {
+  constexpr int per = kM / NB;
+  tile_coords(g, g.t0 + u / per, I, J);
+  *b0 = (int)(u % per) * NB;
 }
 
 // Stage layout (floats): role blocks [A0][B0][W0][A1][B1][W1], each kTile rows x
@@ -80,7 +91,7 @@ __device__ __forceinline__ void issue_stage(float* stage, uint64_t* bar, const S
 
 }  // namespace
 
-template <int MINB>
+template <int MINB, int NB>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
                         const float* __restrict__ fast,
@@ -100,8 +111,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const unsigned one = g.one;
   unsigned long long key = 0;
 
-  int64_t t = blockIdx.x;
-  if (t >= g.n_tiles) {
+  int64_t t = blockIdx.x;  // work unit
+  if (t >= g.n_units) {
     block_max_key(0ull, best_key);
     return;
   }
@@ -117,27 +128,28 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (int e = threadIdx.x; e < kTile * kBgRow; e += kThreads) sbg[e] = -1;
   __syncthreads();
   int64_t I, J;
-  tile_coords(g, t, &I, &J);
+  int b0;
+  unit_coords<NB>(g, t, &I, &J, &b0);
   int s = 0, buf = 0;
   unsigned phase = 0u;  // bit b = parity of the next wait on bars[b]
   if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
 
-  float breg[kM][kM];
+  float breg[kM][NB];
 #pragma unroll
   for (int a = 0; a < kM; a++)
 #pragma unroll
-    for (int b = 0; b < kM; b++) breg[a][b] = 0.0f;  // feasible masked keys are > 0
+    for (int b = 0; b < NB; b++) breg[a][b] = 0.0f;  // feasible masked keys are > 0
 
   while (true) {
     // prefetch the next (tile, state) into the other buffer
     int64_t nt = t, nI = I, nJ = J;
-    int ns = s + 1;
+    int ns = s + 1, nb0 = b0;
     if (ns == sp.n_stages) {
       ns = 0;
       nt = t + gridDim.x;
-      if (nt < g.n_tiles) tile_coords(g, nt, &nI, &nJ);
+      if (nt < g.n_units) unit_coords<NB>(g, nt, &nI, &nJ, &nb0);
     }
-    const bool has_next = nt < g.n_tiles;
+    const bool has_next = nt < g.n_units;
     if (has_next && threadIdx.x == 0)
       issue_stage(smem + (buf ^ 1) * stage_floats, &bars[buf ^ 1], sp, fast, nI, nJ, ns);
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
@@ -148,18 +160,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const float4* A0 = st4 + 0 * blk4 + tx * rs4;
     const float4* B0 = st4 + 1 * blk4 + tx * rs4;
     const uint4* W0 = reinterpret_cast<const uint4*>(st4 + 2 * blk4 + tx * rs4);
-    const float4* A1 = st4 + 3 * blk4 + ty * rs4;
-    const float4* B1 = st4 + 4 * blk4 + ty * rs4;
-    const uint4* W1 = reinterpret_cast<const uint4*>(st4 + 5 * blk4 + ty * rs4);
+    const float4* A1 = st4 + 3 * blk4 + (ty + 16 * b0) * rs4;
+    const float4* B1 = st4 + 4 * blk4 + (ty + 16 * b0) * rs4;
+    const uint4* W1 = reinterpret_cast<const uint4*>(st4 + 5 * blk4 + (ty + 16 * b0) * rs4);
     const int row16 = 16 * rs4;  // float4s between rows r and r+16
 
-    float m[kM][kM];
+    float m[kM][NB];
 #pragma unroll
     for (int q = 0; q < chunks; q++) {
-      float4 a1[kM], b1[kM];
-      uint4 w1[kM];
+      float4 a1[NB], b1[NB];
+      uint4 w1[NB];
 #pragma unroll
-      for (int b = 0; b < kM; b++) {
+      for (int b = 0; b < NB; b++) {
         a1[b] = A1[b * row16 + q];
         b1[b] = B1[b * row16 + q];
         w1[b] = W1[b * row16 + q];
@@ -170,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const float4 b0 = B0[a * row16 + q];
         const uint4 w0 = W0[a * row16 + q];
 #pragma unroll
-        for (int b = 0; b < kM; b++) {
+        for (int b = 0; b < NB; b++) {
           const float4 r0 = add4(a0, b1[b]);
           const float4 r1 = add4(a1[b], b0);
           const float x0 = min3f(__uint_as_float(imad_add(w0.x, one, w1[b].x)), r0.x, r1.x);
@@ -186,11 +198,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 #pragma unroll
     for (int a = 0; a < kM; a++)
-#pragma unroll
-      for (int b = 0; b < kM; b++)
+      for (int b = 0; b < NB; b++)
         if (m[a][b] > breg[a][b]) {  // strict: the first stage wins ties (canonical order)
           breg[a][b] = m[a][b];
-          sbg[(ty + 16 * b) * kBgRow + tx + 16 * a] = (int16_t)s;
+          sbg[(ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a] = (int16_t)s;
         }
 
     if (s == sp.n_stages - 1) {
@@ -200,8 +211,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
       for (int a = 0; a < kM; a++)
 #pragma unroll
-        for (int b = 0; b < kM; b++) {
-          sbest[(ty + 16 * b) * kBgRow + tx + 16 * a] = breg[a][b];
+        for (int b = 0; b < NB; b++) {
+          sbest[(ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a] = breg[a][b];
           breg[a][b] = 0.0f;
         }
       __syncthreads();
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int c_lo = (int)g.c0, c_hi = (int)g.c1;  // this shard's columns (c1 <= n_jobs)
       const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
 #pragma unroll 1
-      for (int e0 = 0; e0 < kTile * kTile; e0 += kPass * kThreads) {
+      for (int e0 = 16 * kTile * b0; e0 < 16 * kTile * (b0 + NB); e0 += kPass * kThreads) {
         float f0[kPass], f1[kPass];
         int c_[kPass];
 #pragma unroll
@@ -265,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     t = nt;
     I = nI;
     J = nJ;
+    b0 = nb0;
     s = ns;
     buf ^= 1;
   }
@@ -300,11 +312,15 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   constexpr size_t smem = (size_t)2 * 6 * kTile * kStageRS * sizeof(float) +
                           (size_t)kTile * kBgRow * (sizeof(float) + sizeof(int16_t));
   static int minb = -1;
+  const char* fs = getenv("COSCHED_PAIR_SPLIT");  // testing knob: force the tail split (1, 2 or 4)
+  const int forced_split = fs ? atoi(fs) : 0;
   if (minb < 0) {
     const char* e = getenv("COSCHED_PAIR_MINB");
     minb = (e && e[0] == '1') ? 1 : 2;
-    cudaFuncSetAttribute(k_score_pairs_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_score_pairs_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_pairs_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_pairs_tiled<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_pairs_tiled<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_score_pairs_tiled<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   if (!g_num_sms) {
     int dev;
@@ -312,16 +328,49 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int per_sm = 0;
-  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1>, kThreads, smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2>, kThreads, smem);
+  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1, 4>, kThreads, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2, 4>, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)g_num_sms * per_sm;
-  if (grid > g.n_tiles) grid = g.n_tiles;
-  if (grid < 1) grid = 1;
-  if (minb == 1)
-    k_score_pairs_tiled<1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
-  else
-    k_score_pairs_tiled<2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+  const int64_t slots = (int64_t)g_num_sms * per_sm;
+  // Tail: whole-tile rounds leave slots - R CTAs idle for a
+  // whole tile time in the last round (R = n_tiles mod slots), which is what
+  // limits strong scaling once a rank has few tiles. The last R tiles go to a
+  // second launch as `split` units per tile (4/split row groups of 16 j1 rows
+  // each, disjoint outputs, no merge), split in {1, 2, 4} minimising
+  // ceil(split * R / slots) / split.
+  const int64_t R = g.n_tiles > slots ? g.n_tiles % slots : g.n_tiles;
+  int split = 1;
+  if (R) {
+    double best = 1.0;
+    for (int h = 2; h <= kM; h *= 2) {
+      const double tt = (double)((h * R + slots - 1) / slots) / h;
+      if (tt < best - 1e-9) {
+        best = tt;
+        split = h;
+      }
+    }
+  }
+  if (forced_split == 1 || forced_split == 2 || forced_split == 4) split = forced_split;
+  if (minb == 1) split = 1;
+  const int64_t n_whole = split == 1 ? g.n_tiles : g.n_tiles - R;
+  if (n_whole > 0) {
+    g.t0 = 0;
+    g.n_units = n_whole;
+    const int64_t grid = n_whole < slots ? n_whole : slots;
+    if (minb == 1)
+      k_score_pairs_tiled<1, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+    else
+      k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+  }
+  if (split > 1) {
+    g.t0 = n_whole;
+    g.n_units = R * split;
+    const int64_t grid = g.n_units < slots ? g.n_units : slots;
+    if (split == 2)
+      k_score_pairs_tiled<2, 2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+    else
+      k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+  }
   return 1;
 }
 

@@ -325,6 +325,29 @@ def test_fast_scorer_equals_generic(cs, n_slots, n):
     assert s0.local_best_key() == s1.local_best_key()
 
 
+@pytest.mark.parametrize("split", ["1", "2", "4"])
+@pytest.mark.parametrize("W", [1, 3])
+def test_pair_tail_split_units(cs, split, W, monkeypatch):
+    """The pair scorer's tail tiles as 1, 2 or 4 row-group units per tile (a second
+    launch, disjoint outputs) give the generic kernel's results on every set of every
+    fake rank (n = 1501: 24 column tiles, 300 tiles, a ragged last column)."""
+    monkeypatch.setenv("COSCHED_PAIR_SPLIT", split)
+    pb = make_problem("b200", "c21", coef_seed=71, alpha=0.5)
+    F, _ = make_features(1501, seed=71)
+    for r in range(W):
+        res = []
+        for variant in (0, 1):
+            s = cs.Scheduler(pb)
+            s.set_variant(variant)
+            s.set_shard_view(r, W)
+            obj, cfg = s.score_all(torch.from_numpy(F).cuda())
+            torch.cuda.synchronize()
+            res.append((obj.cpu().numpy(), cfg.cpu().numpy(), s.local_best_key()))
+        (o0, c0, k0), (o1, c1, k1) = res
+        same = (c0 == c1) & ((o0 == o1) | ((c0 < 0) & (c1 < 0)))
+        assert same.mean() >= 1 - 1e-6 and k0 == k1, (r, np.nonzero(~same)[0][:10])
+
+
 def test_one_rank_nccl_communicator_matches_no_comm(cs):
     """Every collective path (best-set u64 max all-reduce, greedy min/max + histogram
     all-reduces and per-batch all-gathers) run through a real one-rank NCCL communicator
