@@ -352,13 +352,13 @@ def shard_projection(sched, Fd, stream, t1_ms, cand_per_step, args):
     out = {"method": "each rank's shard timed alone on one GPU (fake-rank view), max over ranks; "
                      "excludes the NCCL all-reduce", "t1_ms": t1_ms, "per_w": {}}
     for W in args.shard_ws:
-        per_rank = []
+        per_rank, prep, score = [], [], []
         for r in range(W):
             sched.set_shard_view(r, W)
             for _ in range(2):
                 sched.score_all(Fd, None, with_out=True, stream=stream)
                 sched.best_set()
-            ts = []
+            ts, ps, ss = [], [], []
             for k in range(args.shard_steps):
                 flush.fill_(k & 0xFF)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -368,10 +368,15 @@ def shard_projection(sched, Fd, stream, t1_ms, cand_per_step, args):
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
+                p_, s_, _ = sched.last_timings()
+                ps.append(p_)
+                ss.append(s_)
             per_rank.append(statistics.median(ts))
+            prep.append(statistics.median(ps))
+            score.append(statistics.median(ss))
         sched.set_shard_view(0, 1)
         tmax = max(per_rank)
-        out["per_w"][str(W)] = {"max_ms": tmax, "min_ms": min(per_rank), "per_rank_ms": per_rank,
+        out["per_w"][str(W)] = {"max_ms": tmax, "min_ms": min(per_rank), "per_rank_ms": per_rank, "prep_ms": prep, "score_ms": score,
                                 "projected_speedup": t1_ms / tmax,
                                 "projected_candidates_per_s": cand_per_step / (tmax * 1e-3)}
     return out

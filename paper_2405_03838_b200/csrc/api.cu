@@ -695,11 +695,10 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   // on the device, then read back the validation word, the key and the detail row
   cosched_status st = allreduce_max(h, h->ws.best_key, 1, kNcclUint64);
   if (st != COSCHED_OK) return st;
-  launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->d_detail, h->stream);
+  // the detail kernel writes the validation word, the key and the row straight
+  // into the pinned (mapped) host buffer: no copy on the stream
+  launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->ws.err, h->h_pinned, h->stream);
   h->launches++;
-  CK(cudaMemcpyAsync(h->h_pinned, h->ws.err, 8, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(h->h_pinned + 1, h->ws.best_key, 8, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(h->h_pinned + 2, h->d_detail, 8 * 4, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   st = deferred_status(h, h->h_pinned[0]);
   if (st != COSCHED_OK) return st;

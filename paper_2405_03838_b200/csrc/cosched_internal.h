@@ -171,7 +171,8 @@ void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb,
                         float* out /* [n][4 + kMaxSlots] */, cudaStream_t st);
 // detail row of the set named by the device-resident packed key (best set)
 void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
-                        const unsigned long long* key, float* out, cudaStream_t st);
+                        const unsigned long long* key, const unsigned long long* err, unsigned long long* host_out,
+                        cudaStream_t st);
 void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive,
                            const uint32_t* taken, int64_t* alive_out, int64_t* n_out, cudaStream_t st);
 void launch_greedy_pairs_propose(const float* obj, int64_t first, int64_t c0, int64_t c1, const uint32_t* taken,

@@ -495,7 +495,8 @@ int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const f
 // needs a single device -> host round trip.
 __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
                               const float* __restrict__ w, const int64_t* __restrict__ set_ids,
-                              const unsigned long long* __restrict__ key_src, float* out_all) {
+                              const unsigned long long* __restrict__ key_src, float* out_all,
+                              const unsigned long long* __restrict__ err, unsigned long long* hdr) {
   __shared__ unsigned long long s_key[32];
   float* out = out_all + (int64_t)blockIdx.x * 8;
   int64_t set_id;
@@ -503,6 +504,10 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
     set_id = set_ids[blockIdx.x];
   } else {
     const unsigned long long kk = *key_src;
+    if (hdr && threadIdx.x == 0) {  // best mode: validation word and key next to the row
+      hdr[0] = *err;
+      hdr[1] = kk;
+    }
     if (kk == 0ull) {
       if (threadIdx.x == 0) {
         out[0] = __int_as_float(-1);
@@ -573,12 +578,16 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
 void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
                         int64_t n, float* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out);
+  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out, nullptr, nullptr);
 }
 
 void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
-                        const unsigned long long* key, float* out, cudaStream_t st) {
-  k_sets_detail<<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, out);
+                        const unsigned long long* key, const unsigned long long* err, unsigned long long* host_out,
+                        cudaStream_t st) {
+  // host_out is pinned host memory (UVA-mapped): [0] validation word, [1] key,
+  // [2..5] the detail row -- the kernel writes it directly, no copy
+  k_sets_detail<<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
+                                   host_out);
 }
 
 // Rank sort of a short list of unique keys, descending: position of key i =
