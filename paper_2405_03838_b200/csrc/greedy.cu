@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(1024) k_obj_hist(const float* __restrict__ obj
 // unranking runs at full lane occupancy instead of diverging on every element.
 constexpr int kKirWarps = 8;
 constexpr int kKirQueue = 32 + 4 * 32;
+constexpr int kKirLoads = 4;
 template <int NS>
 __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* __restrict__ obj, int64_t first,
                                                                  int64_t count, const unsigned* __restrict__ mm,
@@ -170,15 +171,24 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   const int64_t n4 = vec4_count(obj, count);
   const float4* o4 = reinterpret_cast<const float4*>(obj);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k0 = gw * 32; k0 < n4; k0 += nw * 32) {
-    const int64_t k = k0 + lane;
-    float4 v = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-    if (k < n4) v = __ldcs(o4 + k);
-    push(in_range(v.x), v.x, first + 4 * k);
-    push(in_range(v.y), v.y, first + 4 * k + 1);
-    push(in_range(v.z), v.z, first + 4 * k + 2);
-    push(in_range(v.w), v.w, first + 4 * k + 3);
-    while (qn >= 32) drain(32);
+  // kKirLoads float4 per lane in flight per iteration (memory-level parallelism:
+  // the queue bookkeeping serialises iterations of a warp)
+  for (int64_t k0 = gw * 32 * kKirLoads; k0 < n4; k0 += nw * 32 * kKirLoads) {
+    float4 v[kKirLoads];
+#pragma unroll
+    for (int u = 0; u < kKirLoads; u++) {
+      const int64_t k = k0 + 32 * u + lane;
+      v[u] = k < n4 ? __ldcs(o4 + k) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < kKirLoads; u++) {
+      const int64_t k = k0 + 32 * u + lane;
+      push(in_range(v[u].x), v[u].x, first + 4 * k);
+      push(in_range(v[u].y), v[u].y, first + 4 * k + 1);
+      push(in_range(v[u].z), v[u].z, first + 4 * k + 2);
+      push(in_range(v[u].w), v[u].w, first + 4 * k + 3);
+      while (qn >= 32) drain(32);
+    }
   }
   // scalar tail (< 4 elements, plus everything when obj is not 16-byte aligned)
   for (int64_t t0 = (n4 << 2) + gw * 32; t0 < count; t0 += nw * 32) {
@@ -454,7 +464,8 @@ void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t 
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
                           unsigned long long* n_keys, cudaStream_t st) {
   if (count <= 0) return;
-  int64_t blocks = std::min<int64_t>((count + 32 * kKirWarps * 4 - 1) / (32 * kKirWarps * 4), 148 * 8);
+  int64_t blocks = std::min<int64_t>((count + 32 * kKirWarps * 4 * kKirLoads - 1) / (32 * kKirWarps * 4 * kKirLoads),
+                                     148 * 8);
   if (n_slots == 2)
     k_keys_in_range<2><<<(unsigned)blocks, 32 * kKirWarps, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi,
                                                                     taken_bits, keys, n_keys);
