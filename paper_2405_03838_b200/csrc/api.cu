@@ -795,9 +795,17 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   int64_t n_picks = 0;
   bool endgame = false;
   while (bin_hi >= 0 && n_picks < k && !endgame) {
+    // only the sets whose jobs are all free are compacted: size the batch on
+    // their expected number, hist x C(n_free, ns) / C(N, ns) (x2 margin across
+    // ranks, whose per-rank capacity is bounded; one rank holds every set)
+    const int64_t n_free0 = N - (int64_t)ns * n_picks;
+    double f_alive = (double)cosched::n_sets(n_free0, ns) / (double)std::max<int64_t>(cosched::n_sets(N, ns), 1);
+    if (h->comm) f_alive = std::min(1.0, 2.0 * f_alive);
+    f_alive = std::max(f_alive, 1.0 / 64.0);
+    const double budget = (double)kBatch / f_alive;
     int bin_lo = bin_hi;
-    int64_t acc = hist[bin_hi];
-    while (bin_lo > 0 && acc + hist[bin_lo - 1] <= kBatch) acc += hist[--bin_lo];
+    double acc = hist[bin_hi];
+    while (bin_lo > 0 && acc + hist[bin_lo - 1] <= budget) acc += hist[--bin_lo];
     if (acc == 0) {
       bin_hi = bin_lo - 1;
       continue;

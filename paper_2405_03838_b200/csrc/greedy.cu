@@ -233,7 +233,9 @@ template <int NS>
 __global__ void k_free_sets(const int32_t* __restrict__ free_list, int64_t n_comb, const float* __restrict__ obj,
                             int64_t first, int64_t count, unsigned long long* keys, unsigned long long* n_keys) {
   const int lane = threadIdx.x & 31;
-  for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; r0 < n_comb; r0 += (int64_t)gridDim.x * blockDim.x) {
+  // a warp covers 32 consecutive ranks (whole-warp ballots); r0 is this warp's first
+  for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; r0 < n_comb;
+       r0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = r0 + lane;
     bool ok = false;
     unsigned long long kk = 0ull;

@@ -112,6 +112,26 @@ def test_c3_greedy_allocation(cs):
     assert all(a >= b for a, b in zip(gk, gk[1:]))
 
 
+@pytest.mark.parametrize("batch", ["3000", "20000", "100000"])
+@pytest.mark.parametrize("table,n,k", [("b200", 600, 300), ("b200_3way", 120, 40)])
+def test_greedy_many_batches_and_endgame(cs, batch, table, n, k, monkeypatch):
+    """Small greedy batches (COSCHED_GREEDY_BATCH) force many histogram batches, the
+    alive-scaled batch sizing and the endgame enumeration of the free jobs' sets: the
+    picks must still replay the oracle's sequential greedy exactly (tie-aware)."""
+    monkeypatch.setenv("COSCHED_GREEDY_BATCH", batch)
+    pb = make_problem(table, "c21", coef_seed=81, alpha=0.2)
+    F, _ = make_features(n, seed=81)
+    ns = pb.n_slots
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    st, ids, cfgs, tot = s.best_allocation(k)
+    _, obj_o = Oracle(pb).score_range(F)
+    ok, why = replay_greedy(n, ns, obj_o, ids)
+    assert ok, why
+    # as many picks as the oracle's greedy finds (it stops only when no disjoint feasible set is left)
+    ref = oracle.greedy_allocation(n, ns, obj_o, k)
+    assert len(ids) == len(ref), (len(ids), len(ref))
+
+
 # ---- edge cases ----------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", [2, 3, 31, 33, 65, 127, 130])
