@@ -857,7 +857,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     // every key whose set touches a job taken meanwhile
     unsigned long long* cur = sorted;
     unsigned long long* spare = h->comm ? ws.gath : (unsigned long long*)ws.alive;
-    const int64_t kChunk = getenv("COSCHED_GREEDY_CHUNK") ? atoll(getenv("COSCHED_GREEDY_CHUNK")) : (1 << 18);
+    const int64_t kChunk = getenv("COSCHED_GREEDY_CHUNK") ? atoll(getenv("COSCHED_GREEDY_CHUNK")) : (1 << 16);
     while (m > 0 && n_picks < k) {
       const int64_t len = std::min<int64_t>(m, kChunk);
       CK(launch_greedy_scan(ns, cur, len, N, taken_bits, ws.picked, np_dev, k, s));
