@@ -196,8 +196,11 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rs = sp.rs, ld = rs + 1, nc = sp.n_caps;
   const size_t npad = (size_t)sp.n_jobs_pad;
-  const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
   unsigned lo = 0xFFFFFFFFu, hi = 0u;
+  // blocks loop over job chunks: the coefficient prologue (dependent global
+  // loads + a block barrier) is paid once per block, not once per 128 jobs
+  for (int64_t chunk = blockIdx.x; chunk * kProjJobs < (int64_t)npad; chunk += gridDim.x) {
+  const int64_t n0 = chunk * kProjJobs + warp * 32, n = n0 + lane;
   if (n0 < (int64_t)npad) {
     float* stg_a = s_stage + warp * 32 * ld;
     float* stg_b = s_stage + (kProjWarps + warp) * 32 * ld;
@@ -236,6 +239,8 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
       __syncwarp();
       flush_rows(stg_a, ld, rs, w + ((((size_t)slot * sp.n_states + state) * npad) + n0) * rs, lane);
     }
+    __syncwarp();  // the staging rows are rewritten by the next chunk
+  }
   }
   if (!is_w) return;
   for (int off = 16; off > 0; off >>= 1) {
@@ -307,9 +312,11 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   if (*err != ~0ull) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t npad = (size_t)sp.n_jobs_pad;
-  const int64_t n0 = (int64_t)blockIdx.x * kProjJobs + warp * 32, n = n0 + lane;
-  if (n0 >= (int64_t)npad) return;
   float* row = s_stage[warp] + lane * ld;
+  // blocks loop over job chunks (the coefficient prologue once per block)
+  for (int64_t chunk = blockIdx.x; chunk * kProjJobs < (int64_t)npad; chunk += gridDim.x) {
+  const int64_t n0 = chunk * kProjJobs + warp * 32, n = n0 + lane;
+  if (n0 >= (int64_t)npad) break;
   const bool job = n < n_jobs;
   float h[6], j[3];
   if (job) load_hj(hj, n, h, j);
@@ -334,6 +341,8 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   __syncwarp();
   static_assert(kStageRS == kStageCfg, "the stage row is exactly the stage's configs");
   flush_rows(s_stage[warp], ld, kStageCfg, fast + (((size_t)role * sp.n_stages + stage) * npad + n0) * kStageRS, lane);
+  __syncwarp();  // the staging rows are rewritten by the next chunk
+  }
 }
 
 __global__ void k_init_wmm(unsigned* wmm) {
@@ -345,7 +354,15 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
                     cudaStream_t st) {
   if (n_jobs <= 0) return;
   k_init_wmm<<<1, 32, 0, st>>>(wmm);
-  const unsigned jb = (unsigned)((sp.n_jobs_pad + kProjJobs - 1) / kProjJobs);
+  // 2 job chunks of 128 per block (measured on C4: 1 -> 60.4 us, 2 -> 58.9,
+  // 4 -> 62.1, 8 -> 75.2 for project + gather; COSCHED_PROJ_CHUNKS overrides)
+  const int64_t n_chunks = (sp.n_jobs_pad + kProjJobs - 1) / kProjJobs;
+  static int per_block = -1;
+  if (per_block < 0) {
+    const char* e = getenv("COSCHED_PROJ_CHUNKS");
+    per_block = e ? std::max(1, atoi(e)) : 2;
+  }
+  const unsigned jb = (unsigned)((n_chunks + per_block - 1) / per_block);
   const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 70 KB (rs <= 68)
   const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
   static bool attr = false;
