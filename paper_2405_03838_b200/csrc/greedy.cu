@@ -126,15 +126,14 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   __shared__ float s_o[kKirWarps][kKirQueue];
   const unsigned lo = mm[0], span = mm[1] - mm[0];
   const unsigned long long u_lo = bin_start(lo, span, bin_lo), u_hi = bin_start(lo, span, bin_hi + 1);  // [u_lo, u_hi)
+  // one 32-bit unsigned compare: u_lo <= hi < 2^32 and u_hi - u_lo <= span + 1 < 2^32;
+  // -inf (infeasible) has ord 0x007FFFFF < lo <= u_lo, so it wraps to a large value
+  const unsigned r_lo = (unsigned)u_lo, r_w = (unsigned)(u_hi - u_lo);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int64_t* qid = s_id[wib];
   float* qo = s_o[wib];
   int qn = 0;  // warp-uniform queue length
-  auto in_range = [&](float o) {
-    if (!(o > -INFINITY)) return false;
-    const unsigned long long u = ord_float_d(o);
-    return u >= u_lo && u < u_hi;
-  };
+  auto in_range = [&](float o) { return ord_float_d(o) - r_lo < r_w; };
   // decode the 32 queue entries [qn - n, qn) (n <= 32), append the free ones
   auto drain = [&](int n) {
     unsigned long long kk = 0ull;
@@ -183,10 +182,12 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
 #pragma unroll
     for (int u = 0; u < kKirLoads; u++) {
       const int64_t k = k0 + 32 * u + lane;
-      push(in_range(v[u].x), v[u].x, first + 4 * k);
-      push(in_range(v[u].y), v[u].y, first + 4 * k + 1);
-      push(in_range(v[u].z), v[u].z, first + 4 * k + 2);
-      push(in_range(v[u].w), v[u].w, first + 4 * k + 3);
+      const bool h0 = in_range(v[u].x), h1 = in_range(v[u].y), h2 = in_range(v[u].z), h3 = in_range(v[u].w);
+      if (!__any_sync(0xFFFFFFFFu, h0 || h1 || h2 || h3)) continue;  // nothing of the warp's 128 in range
+      push(h0, v[u].x, first + 4 * k);
+      push(h1, v[u].y, first + 4 * k + 1);
+      push(h2, v[u].z, first + 4 * k + 2);
+      push(h3, v[u].w, first + 4 * k + 3);
       while (qn >= 32) drain(32);
     }
   }

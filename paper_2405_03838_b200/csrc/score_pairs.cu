@@ -353,7 +353,9 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   if (forced_split == 1 || forced_split == 2 || forced_split == 4) split = forced_split;
   if (minb == 1) split = 1;
   const int64_t n_whole = split == 1 ? g.n_tiles : g.n_tiles - R;
+  int launches = 0;
   if (n_whole > 0) {
+    launches++;
     g.t0 = 0;
     g.n_units = n_whole;
     const int64_t grid = n_whole < slots ? n_whole : slots;
@@ -363,6 +365,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
       k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   }
   if (split > 1) {
+    launches++;
     g.t0 = n_whole;
     g.n_units = R * split;
     const int64_t grid = g.n_units < slots ? g.n_units : slots;
@@ -371,7 +374,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     else
       k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   }
-  return 1;
+  return launches;
 }
 
 }  // namespace cosched
