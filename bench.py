@@ -51,19 +51,59 @@ ALU_LANES_PER_SM_CLK = 64
 N_SM = 148
 
 
-def _traffic(workload: str, n_slots: int):
-    """DRAM bytes per scorer launch from the committed ncu --set full capture
-    (profiles/<round>/<workload>_scorer_ncu_summary.json), or None."""
+def _ncu_summary(workload: str):
+    """The committed ncu --set full summary of the scorer
+    (profiles/<round>/<workload>_scorer_ncu_summary.json), or (None, None)."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"{workload.lower()}_scorer_ncu_summary.json")),
                        reverse=True):
         try:
             with open(path) as f:
-                d = json.load(f)
-            return float(d["traffic_bytes_per_launch"]) / 1e9, os.path.relpath(path, ROOT)
+                return json.load(f), os.path.relpath(path, ROOT)
         except Exception:
             continue
     return None, None
+
+
+def _traffic(workload: str, n_slots: int):
+    """DRAM bytes per scorer launch from the committed ncu --set full capture, or None."""
+    d, src = _ncu_summary(workload)
+    try:
+        return float(d["traffic_bytes_per_launch"]) / 1e9, src
+    except Exception:
+        return None, None
+
+
+def _ncu_pipes(workload: str):
+    """Issue and pipe utilisation of the scorer from the committed ncu capture (SURVEY 8(d):
+    report pipe utilisation and the FMA-FLOP/s against 148 x 128 x 2 x clock)."""
+    d, src = _ncu_summary(workload)
+    if not d:
+        return None
+    keys = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "fmaheavy_pipe_pct": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "lsu_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"}
+    out = {}
+    for k, m in keys.items():
+        try:
+            out[k] = float(d[m])
+        except Exception:
+            pass
+    out["source"] = src
+    return out
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def _peaks():
@@ -92,6 +132,7 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.samples = []  # (sm_mhz, max_mhz, reason bits) from NVML
+        self.power = []    # W, NVML
         self._stop = threading.Event()
         self.t = None
 
@@ -109,6 +150,10 @@ class ClockSampler:
                     try:
                         self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
                                              int(get_reasons(h))))
+                        try:
+                            self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                        except Exception:
+                            pass
                     except Exception:
                         pass
                     time.sleep(0.002)
@@ -151,7 +196,9 @@ class ClockSampler:
             sm = [s[0] for s in self.samples]
             reasons = sorted({name for _, _, bits in self.samples for bit, name in self.REASONS.items() if bits & bit})
             return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                    "reasons": reasons, "samples": len(sm), "source": "NVML, 2 ms polling during the timed steps"}
+                    "reasons": reasons, "samples": len(sm),
+                    "power_w": statistics.median(self.power) if self.power else None,
+                    "source": "NVML, 2 ms polling during the timed steps"}
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -201,7 +248,7 @@ def cpu_oracle_rate(pb, F, n_slots, budget_s=12.0, first=0):
         pool.starmap(_oracle_chunk, [(pb, F, s, chunk) for s in starts])
     dt = time.perf_counter() - t0
     n_cand = cores * chunk * pb.n_configs
-    return {"value": n_cand / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": n_cand / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"{cores} processes x {chunk} consecutive sets ({cores * chunk} sets, "
                       f"{n_cand:.3g} candidates) of {pb.name} with {n_jobs} jobs, single-threaded FP64 "
                       f"un-factorised oracle per process, {dt:.1f} s wall"}
@@ -240,8 +287,8 @@ def run_reference(args):
             "config": {"workload": args.config, "n_jobs": int(F.shape[0]), "n_slots": n_slots,
                        "n_configs": pb.n_configs, "table": pb.name, "objective": pb.objective,
                        "alpha": pb.alpha, "parallelism": "host processes"},
-            "cpu_baseline": {"kind": info["kind"], "cores": info["cores"], "sample": info["sample"],
-                             "value": value, "unit": UNIT},
+            "cpu_baseline": {"kind": info["kind"], "cores": info["cores"], "cpu_model": info.get("cpu_model"),
+                             "sample": info["sample"], "value": value, "unit": UNIT},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -530,7 +577,8 @@ def run_ours(args):
                          "kernel": "set scorer", "ops_per_candidate": ops,
                          "ops_source": "SURVEY.md 8(d) algorithmic FP32 ops per candidate",
                          "kernel_ms": score_avg_ms, "kernel_share_of_step": score_avg_ms / ms_per_step,
-                         "peak_source": f"148 SM x 128 FP32 lanes x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)"},
+                         "peak_source": f"148 SM x 128 FP32 lanes x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)",
+                         "ncu_pipes": _ncu_pipes(args.config)},
             "roofline_strict": {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "T ALU lane-ops/s",
                                 "frac": achieved_alu / alu_peak, "ops_per_candidate": alu_ops,
                                 "ops_source": "ALU-pipe ops the exact method needs per candidate (FMNMX3)",
