@@ -602,6 +602,33 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   launch_fill_u64(ws.err, ~0ull, 1, st);
   launch_fill_u64(ws.best_key, 0ull, 1, st);
   h->launches += 2;
+  {
+    // rows of the gathered layout the tiled scorer reads for this shard: the
+    // sets' largest positions lie in [c0, c1), every other position below c1
+    // (whole-column shards; otherwise every row)
+    int64_t c0 = 0, c1 = n_jobs;
+    const int ns = h->n_slots;
+    auto col_at = [&](int64_t v) {  // smallest c with C(c, ns) >= v
+      int64_t lo = 0, hi = n_jobs;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (cosched::n_sets(mid, ns) >= v) hi = mid;
+        else lo = mid + 1;
+      }
+      return lo;
+    };
+    if (count > 0) {
+      const int64_t a = col_at(first), b = col_at(first + count);
+      if (cosched::n_sets(a, ns) == first && cosched::n_sets(b, ns) == first + count) {
+        c0 = a;
+        c1 = b;
+      }
+    }
+    for (int i = 0; i < kMaxSlots; i++) {
+      h->sp.fast_lo[i] = (i == ns - 1) ? c0 : 0;
+      h->sp.fast_hi[i] = c1;
+    }
+  }
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, ws.hj, st);
     launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
@@ -908,8 +935,9 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
                                            h->d_small_cfg, h->d_small_key, (unsigned long long*)(h->ws.counters + 6),
                                            h->ws.err, h->stream);
     else
+      // every set of the queue: the generic kernel (the gathered layout holds only this shard's rows)
       h->launches += 1 + launch_score(h->sp, N, h->ws.ka, h->ws.kb, h->ws.w, h->ws.fast, 0, all, h->d_small_obj,
-                                      h->d_small_cfg, h->d_small_key, h->ws.err, h->variant, h->stream);
+                                      h->d_small_cfg, h->d_small_key, h->ws.err, 0, h->stream);
     int64_t nm = n_partitions(ns, N);
     launch_exact_alloc(ns, N, h->d_small_obj, nm, h->d_small_key + 1, h->stream);
     launch_exact_unrank(ns, N, h->d_small_key + 1, h->d_small_ids, h->stream);

@@ -54,6 +54,8 @@ struct SpaceParams {
   int32_t search_mode;        // 0 exhaustive, 1 hill climbing from (hc_state, hc_cap) (R22)
   int32_t hc_state, hc_cap;
   float inv_ncaps;            // 1 / n_caps (FP32 division-free config decode in the tile ends)
+  int64_t fast_lo[kMaxSlots], fast_hi[kMaxSlots];  // per slot: job rows of the gathered layout this
+                                                    // rank's tiled scorer reads (gather skips the rest)
   float inv_p[kMaxCaps];      // per cap: fl(1/P) (Problem 2) or 1 (Problem 1)
   int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
 };

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   for (int64_t chunk = blockIdx.x; chunk * kProjJobs < (int64_t)npad; chunk += gridDim.x) {
   const int64_t n0 = chunk * kProjJobs + warp * 32, n = n0 + lane;
   if (n0 >= (int64_t)npad) break;
+  if (n0 + 32 <= sp.fast_lo[slot] || n0 >= sp.fast_hi[slot]) continue;  // rows this rank's scorer never reads
   const bool job = n < n_jobs;
   float h[6], j[3];
   if (job) load_hj(hj, n, h, j);
