@@ -94,6 +94,7 @@ struct cosched_ctx {
   unsigned long long* h_pinned = nullptr;  // [8] pinned host readback
   // last score_all
   bool scored = false;
+  bool kakb_valid = false;  // ka / kb rows of this step's projection present (else launch_project_kakb on demand)
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
   Workspace ws{};
@@ -631,7 +632,13 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   }
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, ws.hj, st);
-    launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, st);
+    // the tiled scorers read only the gathered layout and w: ka / kb are
+    // projected later, and only if a consumer (detail of arbitrary sets, node
+    // budget, exact allocation) asks for them
+    const bool tiled = h->variant != 0 && h->sp.search_mode == 0 && h->n_slots >= 2 &&
+                       (h->n_slots == 3 || (n_jobs + 63) / 64 < 32768);
+    h->kakb_valid = !tiled;
+    launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, !tiled, st);
     h->launches += 4;
   }
   cudaEventRecord(h->ev[1], st);
@@ -701,7 +708,18 @@ cosched_status cosched_local_best_key(cosched_t h, uint64_t* key) {
   return COSCHED_OK;
 }
 
+// The ka / kb rows of the last score_all, if its projection skipped them.
+static void ensure_kakb(cosched_t h) {
+  if (h->kakb_valid) return;
+  if (h->n_jobs > 0) {
+    launch_project_kakb(h->ws.hj, h->n_jobs, h->sp, h->tb, h->ws.err, h->ws.ka, h->ws.kb, h->ws.wmm, h->stream);
+    h->launches++;
+  }
+  h->kakb_valid = true;
+}
+
 static cosched_status detail_rows(cosched_t h, const int64_t* ids, int64_t n, std::vector<float>* rows) {
+  ensure_kakb(h);
   rows->assign((size_t)n * 8, 0.0f);
   for (int64_t off = 0; off < n; off += cosched_ctx::kDetailRows) {
     int64_t m = std::min<int64_t>(cosched_ctx::kDetailRows, n - off);
@@ -724,7 +742,8 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   if (st != COSCHED_OK) return st;
   // the detail kernel writes the validation word, the key and the row straight
   // into the pinned (mapped) host buffer: no copy on the stream
-  launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->ws.err, h->h_pinned, h->stream);
+  launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->ws.err, h->h_pinned, h->ws.hj,
+                     h->kakb_valid ? nullptr : &h->tb, h->stream);
   h->launches++;
   CK(cudaStreamSynchronize(h->stream));
   st = deferred_status(h, h->h_pinned[0]);
@@ -927,6 +946,7 @@ cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids,
   if (ns < 2) return fail(h, COSCHED_E_ARG, "allocation needs n_slots >= 2");
   bool exact = (int64_t)k * ns == N && ((ns == 2 && N <= 20) || (ns == 3 && N <= 15));
   if (exact) {
+    ensure_kakb(h);
     // score every set of the (tiny) queue locally: no collective needed
     int64_t all = cosched::n_sets(N, ns);
     launch_fill_u64(h->d_small_key, 0ull, 2, h->stream);
@@ -1182,6 +1202,7 @@ cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* s
   if (st != COSCHED_OK) return st;
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  ensure_kakb(h);
   int n = node_enqueue(h->sp, h->ws.ka, h->ws.kb, h->ws.w, set_ids, n_gpus, gpus_per_node, U, unit, u.data(),
                        objective, workspace, caps_out, cfgs_out, node_obj, s);
   if (n < 0) return cuda_fail(h, cudaGetLastError(), "node_budget launch");

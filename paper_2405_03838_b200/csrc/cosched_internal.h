@@ -143,7 +143,10 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
                      unsigned long long* err, float* hj, cudaStream_t st);
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
-                    cudaStream_t st);
+                    bool with_kakb, cudaStream_t st);
+// the ka / kb rows alone, after a launch_project without them
+void launch_project_kakb(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
+                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm_scratch, cudaStream_t st);
 // Hill climbing for sets [first, first+count) (search_mode 1); adds the f evaluations to *evals.
 int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                       int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
@@ -174,7 +177,7 @@ void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb,
 // detail row of the set named by the device-resident packed key (best set)
 void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
                         const unsigned long long* key, const unsigned long long* err, unsigned long long* host_out,
-                        cudaStream_t st);
+                        const float* hj, const DeviceTables* tb, cudaStream_t st);
 void launch_greedy_compact(int n_slots, int64_t n_jobs, const int64_t* alive, int64_t n_alive,
                            const uint32_t* taken, int64_t* alive_out, int64_t* n_out, cudaStream_t st);
 void launch_greedy_pairs_propose(const float* obj, int64_t first, int64_t c0, int64_t c1, const uint32_t* taken,

@@ -173,11 +173,11 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
                                                            const float* __restrict__ coef_d,
                                                            const unsigned long long* __restrict__ err,
                                                            float* __restrict__ ka, float* __restrict__ kb,
-                                                           float* __restrict__ w, unsigned* wmm) {
+                                                           float* __restrict__ w, unsigned* wmm, int y0) {
   __shared__ CoefRow s_coef[kMaxCaps];
   __shared__ unsigned s_mm[2];
   extern __shared__ float s_stage[];  // [2][kProjWarps][32][rs + 1]
-  const int y = blockIdx.y;
+  const int y = blockIdx.y + y0;
   const bool is_w = y >= sp.n_slices;
   const int slot = is_w ? (y - sp.n_slices) / sp.n_states : 0, state = is_w ? (y - sp.n_slices) % sp.n_states : 0;
   for (int p = threadIdx.x; p < sp.n_caps; p += blockDim.x) {
@@ -352,7 +352,7 @@ __global__ void k_init_wmm(unsigned* wmm) {
 
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
-                    cudaStream_t st) {
+                    bool with_kakb, cudaStream_t st) {
   if (n_jobs <= 0) return;
   k_init_wmm<<<1, 32, 0, st>>>(wmm);
   // 2 job chunks of 128 per block (measured on C4: 1 -> 60.4 us, 2 -> 58.9,
@@ -365,7 +365,10 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   }
   const unsigned jb = (unsigned)((n_chunks + per_block - 1) / per_block);
   const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 70 KB (rs <= 68)
-  const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
+  // ka / kb rows only when a consumer of this step reads them (the tiled
+  // scorers read the gathered layout and w); launch_project_kakb adds them later
+  const int y0 = with_kakb ? 0 : sp.n_slices;
+  const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states - y0)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_project_all<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
@@ -374,15 +377,35 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
     attr = true;
   }
   if (sp.n_slots == 1) {
-    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
     k_gather_fast<1><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else if (sp.n_slots == 2) {
-    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
     k_gather_fast<2><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else {
-    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm);
+    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
     k_gather_fast<3><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   }
+}
+
+// The ka / kb rows alone (after a launch_project without them).
+void launch_project_kakb(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
+                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm_scratch, cudaStream_t st) {
+  if (n_jobs <= 0) return;
+  const int64_t n_chunks = (sp.n_jobs_pad + kProjJobs - 1) / kProjJobs;
+  const unsigned jb = (unsigned)((n_chunks + 1) / 2);
+  const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);
+  const dim3 gp(jb, (unsigned)sp.n_slices);
+  // the grid covers rows y < n_slices only: the w rows (and wmm) are untouched
+  if (sp.n_slots == 1)
+    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
+                                                         wmm_scratch, 0);
+  else if (sp.n_slots == 2)
+    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
+                                                         wmm_scratch, 0);
+  else
+    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
+                                                         wmm_scratch, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -511,10 +534,71 @@ int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const f
 // set_ids == nullptr: one block for the set named by the packed key *key_src
 // (the best set after the all-reduce; key 0 = none -> cfg -1), so best_set
 // needs a single device -> host round trip.
+// eval_cfg (device_common.cuh) with every operand recomputed from the basis
+// rows hj and the coefficient tables by the projection's own functions: the
+// same FP32 values in the same canonical order, for steps whose projection
+// skipped the ka / kb rows (launch_project with_kakb = false).
+template <int NS>
+__device__ __forceinline__ void eval_cfg_hj(const SpaceParams& sp, const float* __restrict__ hj,
+                                            const float* __restrict__ coef_c, const float* __restrict__ coef_d,
+                                            const int64_t* j, int s, int p, float* r, float* o) {
+  float h[NS][6], jv[NS][3];
+#pragma unroll
+  for (int i = 0; i < NS; i++) load_hj(hj, j[i], h[i], jv[i]);
+  auto KA = [&](int slot_of_slice, int i) {
+    CoefRow cr;
+    load_c(cr, sp, coef_c, sp.slice[s][slot_of_slice], p);
+    return ka_value(sp, cr, h[i]);
+  };
+  auto KB = [&](int slot_of_slice, int i) {
+    CoefRow cr;
+    load_d(cr.d[0], sp, coef_d, sp.slice[s][slot_of_slice], p);
+    return kb_value(cr, jv[i]);
+  };
+  auto WV = [&](int slot) {
+    CoefRow cr;
+    load_w_row(cr, sp, coef_c, coef_d, slot, s, p);
+    return w_value<NS>(cr, h[slot], jv[slot]);
+  };
+  if (NS == 1) {
+    r[0] = KA(0, 0);
+    *o = WV(0);
+  } else if (NS == 2) {
+    r[0] = __fadd_rn(KA(0, 0), KB(0, 1));
+    r[1] = __fadd_rn(KA(1, 1), KB(1, 0));
+    *o = __fadd_rn(WV(0), WV(1));
+  } else {
+    r[0] = __fadd_rn(KA(0, 0), __fadd_rn(KB(0, 1), KB(0, 2)));
+    r[1] = __fadd_rn(__fadd_rn(KA(1, 1), KB(1, 2)), KB(1, 0));
+    r[2] = __fadd_rn(__fadd_rn(KA(2, 2), KB(2, 1)), KB(2, 0));
+    *o = __fadd_rn(WV(0), __fadd_rn(WV(1), WV(2)));
+  }
+}
+
+template <bool HJ>
+__device__ __forceinline__ void eval_any(const SpaceParams& sp, const float* __restrict__ ka,
+                                         const float* __restrict__ kb, const float* __restrict__ w,
+                                         const float* __restrict__ hj, const float* __restrict__ coef_c,
+                                         const float* __restrict__ coef_d, const int64_t* j, int s, int p, float* r,
+                                         float* u) {
+  if (HJ) {
+    if (sp.n_slots == 1) eval_cfg_hj<1>(sp, hj, coef_c, coef_d, j, s, p, r, u);
+    else if (sp.n_slots == 2) eval_cfg_hj<2>(sp, hj, coef_c, coef_d, j, s, p, r, u);
+    else eval_cfg_hj<3>(sp, hj, coef_c, coef_d, j, s, p, r, u);
+  } else {
+    if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, u);
+    else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, u);
+    else eval_cfg<3>(sp, ka, kb, w, j, s, p, r, u);
+  }
+}
+
+template <bool HJ>
 __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
                               const float* __restrict__ w, const int64_t* __restrict__ set_ids,
                               const unsigned long long* __restrict__ key_src, float* out_all,
-                              const unsigned long long* __restrict__ err, unsigned long long* hdr) {
+                              const unsigned long long* __restrict__ err, unsigned long long* hdr,
+                              const float* __restrict__ hj, const float* __restrict__ coef_c,
+                              const float* __restrict__ coef_d) {
   __shared__ unsigned long long s_key[32];
   float* out = out_all + (int64_t)blockIdx.x * 8;
   int64_t set_id;
@@ -554,9 +638,7 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
   for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
     int s = c / sp.n_caps, p = c % sp.n_caps;
     float r[3], u;
-    if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, &u);
-    else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, &u);
-    else eval_cfg<3>(sp, ka, kb, w, j, s, p, r, &u);
+    eval_any<HJ>(sp, ka, kb, w, hj, coef_c, coef_d, j, s, p, r, &u);
     bool feas = true;
     for (int i = 0; i < sp.n_slots; i++) feas = feas && (r[i] > 0.0f);
     unsigned long long kk = feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
@@ -577,9 +659,7 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
     int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
     int s = c / sp.n_caps, p = c % sp.n_caps;
     float thr = 0.0f, fair = INFINITY, u, r[3];
-    if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, &u);
-    else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, &u);
-    else eval_cfg<3>(sp, ka, kb, w, j, s, p, r, &u);
+    eval_any<HJ>(sp, ka, kb, w, hj, coef_c, coef_d, j, s, p, r, &u);
     for (int i = 0; i < sp.n_slots; i++) {
       float rp = __fmaf_rn(r[i], kInvScale, sp.alpha);
       out[4 + i] = rp;
@@ -596,16 +676,22 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
 void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
                         int64_t n, float* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_sets_detail<<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out, nullptr, nullptr);
+  k_sets_detail<false><<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out, nullptr, nullptr, nullptr,
+                                                   nullptr, nullptr);
 }
 
 void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w,
                         const unsigned long long* key, const unsigned long long* err, unsigned long long* host_out,
-                        cudaStream_t st) {
+                        const float* hj, const DeviceTables* tb, cudaStream_t st) {
   // host_out is pinned host memory (UVA-mapped): [0] validation word, [1] key,
-  // [2..5] the detail row -- the kernel writes it directly, no copy
-  k_sets_detail<<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
-                                   host_out);
+  // [2..5] the detail row -- the kernel writes it directly, no copy. tb != NULL:
+  // operands from hj and the coefficient tables (no ka / kb this step)
+  if (tb)
+    k_sets_detail<true><<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
+                                           host_out, hj, tb->coef_c, tb->coef_d);
+  else
+    k_sets_detail<false><<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
+                                            host_out, nullptr, nullptr, nullptr);
 }
 
 // Rank sort of a short list of unique keys, descending: position of key i =

@@ -368,6 +368,24 @@ def test_pair_tail_split_units(cs, split, W, monkeypatch):
         assert same.mean() >= 1 - 1e-6 and k0 == k1, (r, np.nonzero(~same)[0][:10])
 
 
+@pytest.mark.parametrize("table,n", [("b200", 300), ("b200_3way", 60)])
+def test_best_set_detail_from_basis_equals_projection(cs, table, n):
+    """With the tiled scorers the step projects no ka / kb rows: best_set's detail is
+    evaluated from the basis rows and the coefficient tables. It must give exactly the
+    config and objective that best_config (which projects ka / kb on demand and reads
+    them) and the generic scorer give."""
+    pb = make_problem(table, "c21", coef_seed=91, alpha=0.2)
+    F, _ = make_features(n, seed=91)
+    s, obj_g, cfg_g = _run(cs, pb, F)
+    st, sid, cfg, obj = s.best_set()
+    assert st == 0 and cfg == int(cfg_g[sid]) and obj == float(obj_g[sid])
+    d = s.best_config(sid)
+    assert d["cfg"] == cfg and d["obj"] == obj
+    s0, obj0, cfg0 = _run(cs, pb, F, variant=0)
+    st0, sid0, c0, o0 = s0.best_set()
+    assert (sid0, c0, o0) == (sid, cfg, obj)
+
+
 def test_one_rank_nccl_communicator_matches_no_comm(cs):
     """Every collective path (best-set u64 max all-reduce, greedy min/max + histogram
     all-reduces and per-batch all-gathers) run through a real one-rank NCCL communicator
