@@ -165,7 +165,11 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
  * Steps (all kernels): validate features (E_RANGE / E_DEGENERATE_PROFILE for
  * the first bad queue position, reported at the next synchronising call),
  * basis H, J, projection onto C, D, per-set model evaluation, objective,
- * fairness constraint, per-set argmax, per-shard argmax key. */
+ * fairness constraint, per-set argmax, per-shard argmax key. With the tiled
+ * scorers (variant 1, exhaustive mode) the projection's ka / kb rows are not
+ * computed in this call; cosched_best_config, cosched_best_allocation and
+ * cosched_node_budget project them on the same stream when they first need
+ * them (results are identical either way). */
 cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t n_rows,
                                  const int32_t* jobs_dev, int64_t n_jobs, void* workspace_dev,
                                  size_t workspace_bytes, const cosched_out* out, void* cuda_stream);
@@ -176,8 +180,9 @@ cosched_status cosched_local_best_key(cosched_t h, uint64_t* key);
 
 /* COLLECTIVE (when a communicator is set): the queue's best set = max over
  * ranks of the packed key (ncclAllReduce u64 max), then its best config and
- * objective, re-derived on the GPU by its owner... by every rank (the set is
- * recomputed locally from its id; no further exchange).
+ * objective, re-derived on the GPU by every rank from the set id (every rank
+ * holds every job's basis; no further exchange). The detail kernel writes the
+ * result straight into pinned host memory: one stream synchronisation.
  * COSCHED_INFEASIBLE if no set has a feasible config. */
 cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj);
 
@@ -195,8 +200,10 @@ cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, fl
  *    with partners ascending; partitions containing an infeasible set are
  *    skipped; ties -> first in that order;
  *  - greedy otherwise: repeatedly take the feasible set with the largest
- *    (obj, -set_id) whose jobs are all free (computed as parallel
- *    locally-dominant rounds on the GPU), the first k taken.
+ *    (obj, -set_id) whose jobs are all free, the first k taken -- computed on
+ *    the GPU by a histogram-batched sorted scan that resolves the sequential
+ *    rule exactly in parallel rounds (greedy.cu); locally-dominant rounds over
+ *    the shard when a batch exceeds the per-rank capacity.
  * Requires score_all with out != NULL covering the shard.
  * set_ids, cfgs: host arrays of >= k entries; *n_found = sets chosen, in
  * order of formation (exact) or of decreasing key (greedy).
