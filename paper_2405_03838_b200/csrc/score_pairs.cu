@@ -7,17 +7,17 @@
 //   o    = W0[c][j0] + W1[c][j1]              (integer: fixed-point Throughput[/P]
 //                                              with the config's stage offset in the low 5 bits)
 //   x    = min3(float_bits(o), r0'', r1'')    (> 0 iff Fairness > alpha)
-// and the per-pair argmax of x: configs are walked in stages of 24
+// and the per-pair argmax of x: configs are walked in stages of 20 (kStageCfg)
 // along the flattened axis c = state * n_caps + cap (no cap padding); the stage
 // of the best x is kept per pair, its offset comes back from x's low bits, and
 // the winner's exact FP32 objective is read back at tile end.
 //
 // Design (DESIGN.md §5 "Pair scorer"):
-//  - persistent CTAs (two per SM, 16 warps, 128 registers per thread) walk 64x64
+//  - persistent CTAs (two per SM, 8 warps each, 128 registers per thread) walk 64x64
 //    tiles of the pair triangle; each thread owns a 4x4 register micro-tile
 //    (j0 = tx + 16a, j1 = ty + 16b); a warp covers 4 j0 x 8 j1 rows, so every
 //    float4 operand load is one shared-memory wavefront;
-//  - per stage, the tile's operand rows (6 roles x 64 jobs x 28 floats,
+//  - per stage, the tile's operand rows (6 roles x 64 jobs x 20 floats,
 //    contiguous in the gathered layout) land in shared memory by 6 TMA bulk
 //    copies (cp.async.bulk + mbarrier complete_tx), double buffered;
 //  - per 4 caps and pair: 2 FADD2 (r0'', r1''), 4 IMAD (o, FMA pipe),
@@ -25,7 +25,10 @@
 //    candidate, FMA pipe 2 -- the mix that measured fastest in
 //    tools/microbench/inner.cu;
 //  - per stage and pair one FSETP + 2 predicated moves; per tile and pair the
-//    exact FP32 objective of the chosen config (2 loads + 1 FADD).
+//    exact FP32 objective of the chosen config (2 loads + 1 FADD);
+//  - the last round's tiles (n_tiles mod CTA slots) can go to a second launch
+//    as 2 or 4 units of 16-row j1 groups each (k_score_pairs_tiled<MINB, NB>),
+//    chosen to minimise the tail's length.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>

@@ -14,12 +14,15 @@
 // ops (FMNMX + FMNMX3 + half an FMNMX3 for the running max).
 //
 // Tiles: fixed j2, a block of 64 j1 (b) and a block of 64 j0 (a <= b); 256
-// threads, 4 x 4 (j0 x j1) micro-tiles, one resident block per SM. Configs are
-// walked in stages of 24 along the flattened axis (gathered layout, roles
+// threads, 4 x 4 (j0 x j1) micro-tiles, two resident blocks per SM. Configs are
+// walked in stages of 20 along the flattened axis (gathered layout, roles
 // [A0 B01 B02 W0 | A1 B10 B12 W1 | A2 B20 B21 W2]); per stage 8 role blocks of
 // 64 rows and 4 single j2 rows land by TMA bulk copies, double buffered. The
 // stage of each triple's best key is tracked; the offset comes back from the
 // key's low bits and the winner's exact FP32 objective is read back at tile end.
+// The stage body is specialised per tile shape (tstage_body<DIAG, NBV>): diagonal
+// tiles skip the never-valid a > b entries, last-j1-block tiles the row groups
+// at or above j2.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
