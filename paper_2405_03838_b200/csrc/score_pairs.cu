@@ -53,8 +53,14 @@ struct PairGrid {
   int64_t n_tiles;
   int64_t base;       // tiles before the first column tile: jt0*(jt0+1)/2
   int64_t first_set;  // output index offset
-  int64_t t0;         // first tile of this launch
+  int64_t t0;         // first tile of this launch (NB = 4: whole tiles t0 .. t0 + n_units - 1)
   int64_t n_units;    // work units of this launch: a unit is a tile's j1 row groups [b0, b0 + NB)
+  // NB < 4: up to 3 segments of units, segment s covering tiles seg_t0[s]...,
+  // seg_per[s] units per tile starting at row group seg_b[s], units
+  // [seg_end[s-1], seg_end[s]) of the launch
+  int n_seg;
+  int64_t seg_t0[3], seg_end[3];
+  int seg_per[3], seg_b[3];
   unsigned one;       // runtime 1: keeps the integer adds on the FMA pipe (IMAD)
 };
 
@@ -72,9 +78,16 @@ __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_
 // (I, J) and its first row group b0. NB = 4: whole tiles.
 template <int NB>
 __device__ __forceinline__ void unit_coords(const PairGrid& g, int64_t u, int64_t* I, int64_t* J, int* b0) {
-  constexpr int per = kM / NB;
-  tile_coords(g, g.t0 + u / per, I, J);
-  *b0 = (int)(u % per) * NB;
+  if (NB == kM) {
+    tile_coords(g, g.t0 + u, I, J);
+    *b0 = 0;
+    return;
+  }
+  int q = 0;
+  while (q + 1 < g.n_seg && u >= g.seg_end[q]) q++;
+  const int64_t v = u - (q ? g.seg_end[q - 1] : 0);
+  tile_coords(g, g.seg_t0[q] + v / g.seg_per[q], I, J);
+  *b0 = g.seg_b[q] + (int)(v % g.seg_per[q]) * NB;
 }
 
 // Stage layout (floats): role blocks [A0][B0][W0][A1][B1][W1], each kTile rows x
@@ -335,17 +348,49 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2, 4>, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t slots = (int64_t)g_num_sms * per_sm;
+  // Partial column blocks: the shard's first and last column blocks hold only
+  // the 16-row j1 groups [lo0, 4) and [0, hi1) of its columns (a shard boundary
+  // inside a block, or the queue's ragged end); their tiles go to a unit launch
+  // that evaluates only those groups. The other tiles run whole.
+  const int lo0 = (int)((c0 - jt0 * kTile) / 16), hi1 = (int)((c1 - jt1 * kTile + 15) / 16);
+  struct Seg {
+    int64_t t0, n;  // tiles [t0, t0 + n)
+    int groups, b;  // row groups [b, b + groups) of each
+  };
+  Seg segs[3];
+  int n_seg = 0;
+  int64_t fa = 0, fb = g.n_tiles;  // whole tiles [fa, fb)
+  if (minb == 2 && forced_split == 0) {
+    if (jt0 == jt1) {
+      if (hi1 - lo0 < kM) {
+        segs[n_seg++] = {0, g.n_tiles, hi1 - lo0, lo0};
+        fb = fa;
+      }
+    } else {
+      if (lo0 > 0) {
+        segs[n_seg++] = {0, jt0 + 1, kM - lo0, lo0};
+        fa = jt0 + 1;
+      }
+      if (hi1 < kM) {
+        segs[n_seg++] = {g.n_tiles - (jt1 + 1), jt1 + 1, hi1, 0};
+        fb = g.n_tiles - (jt1 + 1);
+      }
+    }
+  }
   // Tail: whole-tile rounds leave slots - R CTAs idle for a
-  // whole tile time in the last round (R = n_tiles mod slots), which is what
-  // limits strong scaling once a rank has few tiles. The last R tiles go to a
-  // second launch as `split` units per tile (4/split row groups of 16 j1 rows
-  // each, disjoint outputs, no merge), split in {1, 2, 4} minimising
-  // ceil(split * R / slots) / split.
-  const int64_t R = g.n_tiles > slots ? g.n_tiles % slots : g.n_tiles;
+  // whole tile time in the last round (R = whole tiles mod slots), which is
+  // what limits strong scaling once a rank has few tiles. The last R whole
+  // tiles can go to the unit launch as `split` units per tile (4/split row
+  // groups of 16 j1 rows each, disjoint outputs, no merge), split in {1, 2, 4}
+  // minimising ceil(split * R / slots) / split; with partial columns the unit
+  // launch has single-group units, so the split is 1 or 4.
+  const int64_t n_full = fb - fa;
+  const int64_t R = n_full > slots ? n_full % slots : n_full;
   int split = 1;
   if (R) {
     double best = 1.0;
     for (int h = 2; h <= kM; h *= 2) {
+      if (n_seg && h != kM) continue;
       const double tt = (double)((h * R + slots - 1) / slots) / h;
       if (tt < best - 1e-9) {
         best = tt;
@@ -355,24 +400,38 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   }
   if (forced_split == 1 || forced_split == 2 || forced_split == 4) split = forced_split;
   if (minb == 1) split = 1;
-  const int64_t n_whole = split == 1 ? g.n_tiles : g.n_tiles - R;
+  const int64_t n_whole = split == 1 ? n_full : n_full - R;
+  const int n_part = n_seg;
+  if (split > 1) segs[n_seg++] = {fa + n_whole, R, kM, 0};
+  const int unit_nb = (n_part == 0 && split == 2) ? 2 : 1;  // row groups per unit of the unit launch
   int launches = 0;
   if (n_whole > 0) {
     launches++;
-    g.t0 = 0;
+    g.t0 = fa;
     g.n_units = n_whole;
+    g.n_seg = 0;
     const int64_t grid = n_whole < slots ? n_whole : slots;
     if (minb == 1)
       k_score_pairs_tiled<1, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
     else
       k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   }
-  if (split > 1) {
+  if (n_seg > 0) {
     launches++;
-    g.t0 = n_whole;
-    g.n_units = R * split;
-    const int64_t grid = g.n_units < slots ? g.n_units : slots;
-    if (split == 2)
+    int64_t end = 0;
+    for (int q = 0; q < n_seg; q++) {
+      const int per = segs[q].groups / unit_nb;  // units per tile
+      end += segs[q].n * per;
+      g.seg_t0[q] = segs[q].t0;
+      g.seg_end[q] = end;
+      g.seg_per[q] = per;
+      g.seg_b[q] = segs[q].b;
+    }
+    g.n_seg = n_seg;
+    g.t0 = 0;
+    g.n_units = end;
+    const int64_t grid = end < slots ? end : slots;
+    if (unit_nb == 2)
       k_score_pairs_tiled<2, 2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
     else
       k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
