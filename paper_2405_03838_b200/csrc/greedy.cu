@@ -293,12 +293,13 @@ __global__ void __launch_bounds__(1024, 1)
   constexpr int WIN = 1024 * CPT;
   extern __shared__ uint32_t s_dyn[];
   uint32_t* s_taken = s_dyn;                                                    // n_jobs bits
-  int32_t* s_first = reinterpret_cast<int32_t*>(s_dyn + ((n_jobs + 31) >> 5));  // n_jobs
+  uint32_t* s_first = s_dyn + ((n_jobs + 31) >> 5);  // n_jobs: round-stamped claims
   __shared__ int32_t s_wsum[32];
   __shared__ int64_t s_np;
   const int words = (int)((n_jobs + 31) >> 5);
   for (int i = threadIdx.x; i < words; i += blockDim.x) s_taken[i] = taken_g[i];
-  for (int i = threadIdx.x; i < n_jobs; i += blockDim.x) s_first[i] = 0x7FFFFFFF;
+  for (int i = threadIdx.x; i < n_jobs; i += blockDim.x) s_first[i] = 0u;
+  unsigned rnd = 1;  // round stamp (< 2^20 rounds per launch)
   if (threadIdx.x == 0) s_np = *n_picks;
   __syncthreads();
   const int t = threadIdx.x;
@@ -333,46 +334,50 @@ __global__ void __launch_bounds__(1024, 1)
         }
       }
     }
+    // rounds: every undecided key claims its jobs with a round-stamped
+    // atomicMax of (round << 12 | 4095 - index); a key that holds the claim on
+    // all its jobs is the lowest undecided key on each of them, so the
+    // sequential rule takes it. Stamps grow with the round, so the claims of
+    // earlier rounds never need resetting: two barriers per round.
     bool any = false;
 #pragma unroll
     for (int u = 0; u < CPT; u++) any = any || und[u];
-    while (__syncthreads_or(any)) {
+    if (__syncthreads_or(any)) {
+      bool cont = true;
+      while (cont) {
+        const unsigned stamp = rnd << 12;
 #pragma unroll
-      for (int u = 0; u < CPT; u++)
-        if (und[u])
+        for (int u = 0; u < CPT; u++)
+          if (und[u])
 #pragma unroll
-          for (int q = 0; q < NS; q++) atomicMin(&s_first[jb[u][q]], t * CPT + u);
-      __syncthreads();
-      bool take[CPT];
+            for (int q = 0; q < NS; q++) atomicMax(&s_first[jb[u][q]], stamp | (unsigned)(WIN - 1 - (t * CPT + u)));
+        __syncthreads();
+        bool left = false;
 #pragma unroll
-      for (int u = 0; u < CPT; u++) {
-        take[u] = und[u];
-        if (und[u])
+        for (int u = 0; u < CPT; u++) {
+          if (!und[u]) continue;
+          const unsigned mine = stamp | (unsigned)(WIN - 1 - (t * CPT + u));
+          bool take = true;
 #pragma unroll
-          for (int q = 0; q < NS; q++) take[u] = take[u] && (s_first[jb[u][q]] == t * CPT + u);
-      }
-      __syncthreads();
+          for (int q = 0; q < NS; q++) take = take && (s_first[jb[u][q]] == mine);
+          if (take) {
 #pragma unroll
-      for (int u = 0; u < CPT; u++) {
-        if (und[u])
-#pragma unroll
-          for (int q = 0; q < NS; q++) s_first[jb[u][q]] = 0x7FFFFFFF;  // reset for the next round
-        if (take[u]) {
-#pragma unroll
-          for (int q = 0; q < NS; q++) atomicOr(&s_taken[jb[u][q] >> 5], 1u << (jb[u][q] & 31));
-          acc[u] = true;
-          und[u] = false;
+            for (int q = 0; q < NS; q++) atomicOr(&s_taken[jb[u][q] >> 5], 1u << (jb[u][q] & 31));
+            acc[u] = true;
+            und[u] = false;
+          }
+          left = left || und[u];
         }
-      }
-      __syncthreads();
-      any = false;
+        rnd++;
+        cont = __syncthreads_or(left);  // every taken bit of this round is visible after it
+        if (cont) {
 #pragma unroll
-      for (int u = 0; u < CPT; u++) {
-        if (und[u])
+          for (int u = 0; u < CPT; u++)
+            if (und[u])
 #pragma unroll
-          for (int q = 0; q < NS; q++)
-            if ((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u) und[u] = false;
-        any = any || und[u];
+              for (int q = 0; q < NS; q++)
+                if ((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u) und[u] = false;
+        }
       }
     }
     // emit the window's picks in index order (block prefix sum), stopping at k_max
