@@ -363,25 +363,32 @@ def hill_metrics(sched, Fd, pb, stream, args):
     import torch
     obj_e, cfg_e = sched.score_all(Fd, None, with_out=True, stream=stream)
     obj_e, cfg_e = obj_e.clone(), cfg_e.clone()
-    start = (0, pb.n_caps - 1)
-    sched.set_search(1, *start)
-    times = []
-    for _ in range(2):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        obj_h, cfg_h = sched.score_all(Fd, None, with_out=True, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    evals = sched.last_search_evals()
-    feas = (cfg_e >= 0) & (cfg_h >= 0)
-    ratio = (obj_h[feas].double() / obj_e[feas].double())
-    out = {"start": {"state": start[0], "cap": start[1]}, "ms": min(times), "sets": int(cfg_e.numel()),
-           "evals": int(evals), "evals_per_set": evals / max(cfg_e.numel(), 1),
-           "evals_per_s": evals / (min(times) * 1e-3),
-           "same_config_as_exhaustive": float((cfg_h == cfg_e).double().mean().item()),
-           "objective_ratio_mean": float(ratio.mean().item()) if ratio.numel() else None,
-           "objective_ratio_geomean": float(torch.exp(torch.log(ratio).mean()).item()) if ratio.numel() else None}
+
+    def climb(start):
+        sched.set_search(1, *start)
+        times = []
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            obj_h, cfg_h = sched.score_all(Fd, None, with_out=True, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        evals = sched.last_search_evals()
+        feas = (cfg_e >= 0) & (cfg_h >= 0)
+        ratio = (obj_h[feas].double() / obj_e[feas].double())
+        return {"start": {"state": int(start[0]), "cap": int(start[1])}, "ms": min(times), "sets": int(cfg_e.numel()),
+                "evals": int(evals), "evals_per_set": evals / max(cfg_e.numel(), 1),
+                "evals_per_s": evals / (min(times) * 1e-3),
+                "same_config_as_exhaustive": float((cfg_h == cfg_e).double().mean().item()),
+                "objective_ratio_mean": float(ratio.mean().item()) if ratio.numel() else None,
+                "objective_ratio_geomean": float(torch.exp(torch.log(ratio).mean()).item()) if ratio.numel() else None}
+
+    # the first state of the table at P_max, and the most even split (the first
+    # state with the smallest largest slot, shared memory) at P_max
+    out = climb((0, pb.n_caps - 1))
+    balanced = int(np.argmin(np.asarray(pb.state_gpcs).max(axis=1)))
+    out["balanced_start"] = climb((balanced, pb.n_caps - 1))
     sched.set_search(0)
     return out
 
