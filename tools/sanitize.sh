@@ -20,6 +20,10 @@ for table, n in (("b200", 130), ("b200_3way", 40)):
     s.node_budget(ids, 4, 3000.0, 2)
     s.set_search(1, 0, 0); s.score_all(Fd); s.best_set()
     s.set_variant(0); s.set_search(0); s.score_all(Fd)
+    s.set_variant(1)
+    for r in range(3):  # fake-rank shards: partial boundary column blocks, row-sharded gather
+        s.set_shard_view(r, 3); s.score_all(Fd); s.best_set()
+    s.set_shard_view(0, 1)
 pb, F = bench_config("C2")
 ts = make_training_set(F, pb, n_corun=100, seed=1)
 d = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
