@@ -597,6 +597,16 @@ def run_ours(args):
             "node_budget": node_info,
             "clocks": clocks,
         }
+        # the paper's own selection-quality numbers, quoted with their hardware
+        # (context only, not comparable: A100 measurements of 18 real pairs)
+        line["paper_context"] = {
+            "hardware": "NVIDIA A100 40GB PCIe, Threadripper PRO 3955WX, CUDA 11.5 (PAPER.md L503-519)",
+            "problem1_geomean_weighted_speedup_proposal_vs_best": [1.52, 1.54],
+            "problem1_setting": "P = 230 W, alpha = 0.2, 18 pairs (PAPER.md L754, 5.2.2)",
+            "model_mean_abs_rel_error_throughput_fairness": [0.097, 0.145],
+            "model_error_source": "PAPER.md L742 (5.2.1)",
+            "fairness_violations": 0,
+            "our_analogue": "calibration.pipeline: geomean proposal/best on the synthetic-GPU ground truth"}
         if args.shard_ws and world == 1:
             line["shard_projection"] = shard_projection(sched, Fd, stream, ms_per_step, cand_per_step, args)
         if args.hill:
