@@ -115,7 +115,11 @@ const char* cosched_last_create_error(void);
  * exchanges are the argmax all-reduces of cosched_best_set /
  * cosched_best_allocation, done with ncclAllReduce(u64, max) on the
  * library's own communicator. NCCL is loaded at run time (dlopen
- * "libnccl.so.2", the copy torch already loaded when present). */
+ * "libnccl.so.2", the copy torch already loaded when present). Test hook:
+ * when the environment variable COSCHED_NCCL_LIB names a library exporting the
+ * same six NCCL entry points, that library is loaded instead (read once per
+ * process, at the first communicator use); tests/loopback/ provides an
+ * in-process stand-in that runs W ranks as W threads on one GPU. */
 
 /* Rank 0: write a 128-byte ncclUniqueId to uid_out (host). E_NCCL if NCCL is unavailable. */
 cosched_status cosched_get_unique_id(void* uid_out);
@@ -165,7 +169,14 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
  * Steps (all kernels): validate features (E_RANGE / E_DEGENERATE_PROFILE for
  * the first bad queue position, reported at the next synchronising call),
  * basis H, J, projection onto C, D, per-set model evaluation, objective,
- * fairness constraint, per-set argmax, per-shard argmax key. With the tiled
+ * fairness constraint, per-set argmax, per-shard argmax key.
+ * Exactness: out->cfg[k] is the exact FP32 argmax of set k (strict >, lowest
+ * config on ties) or a config whose FP32 objective is within tau/2 = 5e-6
+ * relative of it, for every valid input; out->obj[k] is the FP32 objective of
+ * out->cfg[k] (-inf, cfg -1 iff no config is feasible: feasibility is decided
+ * exactly). The tiled scorers compare configs by a fixed-point objective and
+ * re-score exactly, in the same call, every set where that could miss the
+ * bound (cosched_last_rescored). With the tiled
  * scorers (variant 1, exhaustive mode) the projection's ka / kb rows are not
  * computed in this call; cosched_best_config, cosched_best_allocation and
  * cosched_node_budget project them on the same stream when they first need
@@ -181,8 +192,10 @@ cosched_status cosched_local_best_key(cosched_t h, uint64_t* key);
 /* COLLECTIVE (when a communicator is set): the queue's best set = max over
  * ranks of the packed key (ncclAllReduce u64 max), then its best config and
  * objective, re-derived on the GPU by every rank from the set id (every rank
- * holds every job's basis; no further exchange). The detail kernel writes the
- * result straight into pinned host memory: one stream synchronisation.
+ * holds every job's basis; no further exchange). *cfg and *obj are that set's
+ * exact FP32 argmax and its objective (the detail kernel's evaluation). The
+ * detail kernel writes the result straight into pinned host memory: one
+ * stream synchronisation.
  * COSCHED_INFEASIBLE if no set has a feasible config. */
 cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj);
 
@@ -303,6 +316,17 @@ cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* s
  * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */
 cosched_status cosched_last_timings(cosched_t h, float* ms3);
+
+/* Sets of the last cosched_score_all that the tiled scorer flagged for exact
+ * re-scoring (instrumentation): those whose packed-objective choice was not
+ * provably within tau/2 = 5e-6 relative of the exact FP32 argmax (objective
+ * below 6 * n_slots quanta / tau; DESIGN.md §2 "Exactness of the tiled argmax").
+ * (Pairs: the sets the tile end flagged, or more than the list holds; triples:
+ * the sets the objective scan found.)
+ * Every flagged set was re-scored exactly by k_rescore_sets in the same call, so
+ * this is a performance counter, not an error. 0 with the generic scorer.
+ * Synchronises the stream. */
+cosched_status cosched_last_rescored(cosched_t h, int64_t* n_rescored);
 
 /* Rounds of the last greedy cosched_best_allocation (instrumentation). */
 int64_t cosched_last_greedy_rounds(cosched_t h);

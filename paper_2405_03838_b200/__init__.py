@@ -159,6 +159,13 @@ class Scheduler:
         return int(self._L.cosched_last_greedy_rounds(self._h))
 
     @property
+    def last_rescored(self) -> int:
+        """Sets of the last score_all re-scored exactly after the tiled scorer (instrumentation)."""
+        n = ctypes.c_int64()
+        self._check(self._L.cosched_last_rescored(self._h, ctypes.byref(n)))
+        return n.value
+
+    @property
     def kernel_launches(self) -> int:
         return int(self._L.cosched_kernel_launches(self._h))
 

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("cosched_last_timings", I32, [P, P]),
     ("cosched_kernel_launches", I64, [P]),
     ("cosched_last_greedy_rounds", I64, [P]),
+    ("cosched_last_rescored", I32, [P, P]),
     ("cosched_node_workspace_size", I32, [P, I64, I32, ctypes.c_double, P]),
     ("cosched_node_budget", I32, [P, I64, P, I32, ctypes.c_double, I32, P, ctypes.c_size_t, P, P, P, P]),
     ("cosched_evaluate_workspace_size", I32, [P, I64, P]),

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -41,11 +42,22 @@ struct NcclApi {
 NcclApi g_nccl;
 
 bool nccl_load(std::string* why) {
+  static std::mutex mu;  // handles of one process may bootstrap from several threads
+  std::lock_guard<std::mutex> lk(mu);
   if (!g_nccl.tried) {
     g_nccl.tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // COSCHED_NCCL_LIB: another library with the same six entry points (the
+    // test-only in-process loopback, tests/loopback/, runs W ranks as W threads
+    // on one GPU); read once, at the first communicator use of the process
+    const char* alt = getenv("COSCHED_NCCL_LIB");
+    void* h = nullptr;
+    if (alt && alt[0]) {
+      h = dlopen(alt, RTLD_NOW | RTLD_LOCAL);
+    } else {
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    }
     if (h) {
       g_nccl.getUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
       g_nccl.commInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
@@ -182,6 +194,14 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   const int64_t list_max = std::max<int64_t>(nranks > 0 ? gathered : n_sets_local, 1);
   w.sort_tmp_bytes = std::max(sort_temp_bytes(list_max), select_temp_bytes(list_max));
   w.sort_tmp = take(w.sort_tmp_bytes);
+  // exact re-scoring list of the tiled scorers: normally empty; an
+  // overflow re-scores every flagged-range set instead, so the capacity is a
+  // memory bound, not a correctness one
+  int64_t rcap = (int64_t)1 << 20;
+  if (const char* e = getenv("COSCHED_RESCORE_CAP")) rcap = std::max<int64_t>(0, atoll(e));  // testing knob: overflow path
+  w.rescore_cap = (unsigned)std::min<int64_t>(std::max<int64_t>(n_sets_local, 1), rcap);
+  w.rescore_list = (unsigned*)take((size_t)std::max<unsigned>(w.rescore_cap, 1u) * 4);
+  w.rescore_n = (unsigned*)take(8);
   w.bytes = off;
   if (ws) *ws = w;
   return off;
@@ -378,6 +398,17 @@ const char* cosched_last_error(cosched_t h) { return h ? h->err.c_str() : g_crea
 int64_t cosched_kernel_launches(cosched_t h) { return h ? h->launches : 0; }
 
 int64_t cosched_last_greedy_rounds(cosched_t h) { return h ? h->greedy_rounds : 0; }
+
+cosched_status cosched_last_rescored(cosched_t h, int64_t* n_rescored) {
+  if (!h || !n_rescored) return fail(h, COSCHED_E_ARG, "null argument");
+  if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  DeviceGuard g(h->device);
+  unsigned v = 0;
+  CK(cudaMemcpyAsync(&v, h->ws.rescore_n, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  *n_rescored = (int64_t)v;
+  return COSCHED_OK;
+}
 
 cosched_status cosched_set_variant(cosched_t h, int variant) {
   if (!h || variant < 0 || variant > 1) return COSCHED_E_ARG;
@@ -600,9 +631,8 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 0, (char*)workspace_dev, &ws);
   h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
-  launch_fill_u64(ws.err, ~0ull, 1, st);
-  launch_fill_u64(ws.best_key, 0ull, 1, st);
-  h->launches += 2;
+  launch_step_init(ws.err, ws.best_key, ws.rescore_n, ws.wmm, st);
+  h->launches += 1;
   {
     // rows of the gathered layout the tiled scorer reads for this shard: the
     // sets' largest positions lie in [c0, c1), every other position below c1
@@ -635,11 +665,10 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     // the tiled scorers read only the gathered layout and w: ka / kb are
     // projected later, and only if a consumer (detail of arbitrary sets, node
     // budget, exact allocation) asks for them
-    const bool tiled = h->variant != 0 && h->sp.search_mode == 0 && h->n_slots >= 2 &&
-                       (h->n_slots == 3 || (n_jobs + 63) / 64 < 32768);
+    const bool tiled = h->variant != 0 && h->sp.search_mode == 0 && tiled_applicable(h->n_slots, n_jobs, first, count);
     h->kakb_valid = !tiled;
     launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, !tiled, st);
-    h->launches += 4;
+    h->launches += 3;
   }
   cudaEventRecord(h->ev[1], st);
   if (h->sp.search_mode == 1) {
@@ -647,8 +676,13 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     h->launches += 1 + launch_score_hill(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key,
                                          (unsigned long long*)(ws.counters + 7), ws.err, st);
   } else {
+    RescoreBuf rb;
+    rb.wmm = ws.wmm;
+    rb.list = ws.rescore_list;
+    rb.n = ws.rescore_n;
+    rb.cap = ws.rescore_cap;
     h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
-                                ws.err, h->variant, st);
+                                ws.err, h->variant, st, rb);
   }
   cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
@@ -756,7 +790,11 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   if (obj) *obj = o;
   if (cfg) *cfg = -1;
   if (key == 0) return COSCHED_INFEASIBLE;
+  // config and objective of the same evaluation: the detail row's exact FP32
+  // argmax of the winning set (the key's objective can be the packed-objective
+  // choice, within tau/2 of it)
   if (cfg) memcpy(cfg, h->h_pinned + 2, 4);
+  if (obj) memcpy(obj, reinterpret_cast<const float*>(h->h_pinned + 2) + 1, 4);
   return COSCHED_OK;
 }
 

@@ -60,6 +60,16 @@ struct SpaceParams {
   int16_t slice[kMaxStates][kMaxSlots];  // state -> slice per slot
 };
 
+// Exact re-scoring of the sets whose packed-objective choice is not provably
+// within tau/2 of the FP32 argmax (device_common.cuh rescore_threshold): the
+// tiled scorers' tile ends append the local index of such a set to `list`.
+struct RescoreBuf {
+  const unsigned* wmm = nullptr;  // [2 * kMaxSlots] per-slot share ranges (the quantum, hence the threshold)
+  unsigned* list = nullptr;       // [cap] flagged local set indices (k = set id - first)
+  unsigned* n = nullptr;          // [1] number flagged; > cap: every set below the threshold is re-scored
+  unsigned cap = 0;
+};
+
 // Device-side tables owned by a handle.
 struct DeviceTables {
   float* coef_c = nullptr;  // [n_caps][n_slices][6]
@@ -93,6 +103,9 @@ struct Workspace {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   int64_t batch_cap = 0;                   // keys per rank per greedy batch
+  unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
+  unsigned* rescore_n = nullptr;           // [1]
+  unsigned rescore_cap = 0;
   size_t bytes = 0;
 };
 
@@ -153,9 +166,25 @@ int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, co
                       unsigned long long* evals, const unsigned long long* err, cudaStream_t st);
 // Scores sets [first, first+count) of the queue; writes obj/cfg (may be null) and atomically
 // maxes the packed key into *best_key. Returns the number of kernels launched.
+// variant 0: the generic one-thread-per-set kernel (reads ka / kb / w); variant 1: the
+// tiled scorers (read the gathered layout and w) plus the exact re-scoring of the
+// flagged sets (rb), when tiled_applicable(), else the generic kernel.
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                 const unsigned long long* err, int variant, cudaStream_t st);
+                 const unsigned long long* err, int variant, cudaStream_t st, const RescoreBuf& rb = RescoreBuf());
+// Whether the tiled scorer takes shard [first, first + count) of an n_jobs queue
+// (whole colex columns / planes; pair queues below 32768 column tiles). The one
+// place the tiled-or-generic decision is made: score_all projects ka / kb for
+// the generic kernel exactly when this is false.
+bool tiled_applicable(int n_slots, int64_t n_jobs, int64_t first, int64_t count);
+// Per-device, thread-safe opt-in to more than 48 KB of dynamic shared memory
+// for `func` (a __global__ function), done once per (function, device, size);
+// returns the CUDA error of the opt-in. num_sms(): SMs of the current device.
+cudaError_t smem_optin(const void* func, size_t bytes);
+int num_sms();
+// Step start: err = ~0 (valid), best_key = 0, rescore count = 0, wmm = empty ranges.
+void launch_step_init(unsigned long long* err, unsigned long long* best_key, unsigned* rescore_n, unsigned* wmm,
+                      cudaStream_t st);
 void launch_exact_alloc(int n_slots, int64_t n_jobs, const float* set_obj, int64_t n_match,
                         unsigned long long* best_key, cudaStream_t st);
 void launch_exact_unrank(int n_slots, int64_t n_jobs, const unsigned long long* best_key, int64_t* set_ids,

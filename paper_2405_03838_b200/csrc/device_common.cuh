@@ -138,6 +138,34 @@ __device__ __forceinline__ float unord_float_d(uint32_t o) {
   return __uint_as_float(b);
 }
 
+// ---- packed objective of the tiled scorers ----
+// Inverse quantum inv = (2^25 - 2 - NS) / sum_i (wmax_i - wmin_i) from the
+// per-slot ranges wmm (order-preserving u32, k_project_all); 0 when every share
+// is equal (then every packed objective ties and the canonical order decides).
+template <int NS>
+__device__ __forceinline__ float quant_inv(const unsigned* __restrict__ wmm) {
+  float span = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NS; i++) span += unord_float_d(wmm[2 * i + 1]) - unord_float_d(wmm[2 * i]);
+  return span > 0.0f ? (float)(33554430 - NS) / span : 0.0f;
+}
+
+// Exactness bound of the packed argmax (DESIGN.md §2 "Exactness of the tiled
+// argmax"). Each slot's code q = rint(fma(w, inv, -fl(lo*inv))) is within 1.5
+// quanta of inv*w + const_slot (one FMA rounding <= 1 below 2^25, rint 0.5), so a
+// candidate's packed key is within 1.5*NS quanta of inv*(sum of its FP32 shares)
+// + const, and the config the max picks has a true FP32 objective at most
+// 3*NS/inv below the set's FP32 maximum. Sets whose chosen objective O satisfies
+// 3*NS/inv > (tau/2)*O, i.e. O < 6*NS/(tau*inv), are re-scored exactly
+// (k_rescore_sets): every reported choice is within tau/2 = 5e-6 relative of the
+// exact FP32 argmax's objective, whatever the input.
+constexpr float kTauObj = 1e-5f;  // BASELINE.json north_star: objectives within 1e-5 relative
+template <int NS>
+__device__ __forceinline__ float rescore_threshold(const unsigned* __restrict__ wmm) {
+  const float inv = quant_inv<NS>(wmm);
+  return inv > 0.0f ? (6.0f * NS / kTauObj) / inv : 0.0f;
+}
+
 // Packed argmax key: larger objective first, then lower set id. Unique per set.
 __device__ __forceinline__ unsigned long long pack_key(float obj, int64_t sid) {
   return ((unsigned long long)ord_float_d(obj) << 32) | (0xFFFFFFFFull - (unsigned long long)(uint32_t)sid);

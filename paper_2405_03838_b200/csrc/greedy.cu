@@ -460,11 +460,7 @@ void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream
 }
 void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st) {
   if (count <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_obj_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistBins * 4);
-    attr = true;
-  }
+  smem_optin((const void*)k_obj_hist, kHistBins * 4);
   int64_t blocks = std::min<int64_t>((count + 1023) / 1024, 148 * 2);
   k_obj_hist<<<(unsigned)blocks, 1024, kHistBins * 4, st>>>(obj, count, mm, nbins, hist);
 }

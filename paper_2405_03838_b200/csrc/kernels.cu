@@ -13,6 +13,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "cosched_internal.h"
 #include "device_common.cuh"
@@ -103,6 +106,7 @@ struct CoefRow {
   float c[6];                   // C[p][slice of the slot]
   float d[kMaxSlots][3];        // D[p][slice]: [0] for a kb row; for a w row D of the other slots, ascending
   float inv_p;
+  float wfloor;                 // w row: below this share every config is infeasible (feasibility floor)
 };
 __device__ __forceinline__ void load_c(CoefRow& r, const SpaceParams& sp, const float* __restrict__ coef_c, int slice,
                                        int p) {
@@ -114,14 +118,39 @@ __device__ __forceinline__ void load_d(float d[3], const SpaceParams& sp, const 
 #pragma unroll
   for (int t = 0; t < 3; t++) d[t] = __ldg(coef_d + ((int64_t)p * sp.n_slices + slice) * 3 + t);
 }
-// w row of (slot, state s) at cap p: C of the slot's slice, D of the other slots' slices
+// Bounds of V = D.J over valid features: J = (F3/100, F4/100, 1) with F3, F4 in
+// [0, 100] (a1), so J1, J2 in [0, 1] and V lies in [d3 + min(d1,0) + min(d2,0),
+// d3 + max(d1,0) + max(d2,0)].
+__device__ __forceinline__ float vmax_of(const float d[3]) { return d[2] + fmaxf(d[0], 0.0f) + fmaxf(d[1], 0.0f); }
+__device__ __forceinline__ float vmin_of(const float d[3]) { return d[2] + fminf(d[0], 0.0f) + fminf(d[1], 0.0f); }
+
+// w row of (slot, state s) at cap p: C of the slot's slice, D of the other slots' slices.
+// Feasibility floor (DESIGN.md §2 "Exactness of the tiled argmax"): a feasible
+// config has RPerf_i = U_i[s_i] + sum_{l!=i} V_l[s_i] > alpha, so U_i[s_i] >
+// alpha - (NS-1) Vmax[s_i], and w_i = (U_i[s_i] + sum_{l!=i} V_i[s_l]) / P >
+// (alpha - (NS-1) Vmax[s_i] + sum_{l!=i} Vmin[s_l]) / P. Shares below that
+// (minus a slack far above the FP32 rounding of these O(1) sums) belong to
+// infeasible configs only, so they are left out of the quantisation range and
+// coded as its bottom: one extreme but valid profile (F1 near 0.01 %, H3 = F2/F1
+// up to 10^4) cannot coarsen the packed objective of the whole queue.
 __device__ __forceinline__ void load_w_row(CoefRow& r, const SpaceParams& sp, const float* __restrict__ coef_c,
                                            const float* __restrict__ coef_d, int slot, int s, int p) {
   load_c(r, sp, coef_c, sp.slice[s][slot], p);
+  float own[3];
+  load_d(own, sp, coef_d, sp.slice[s][slot], p);
+  const float vmx = vmax_of(own);
+  float f = sp.alpha, mag = 1.0f + fabsf(sp.alpha);
   int k = 0;
   for (int l = 0; l < sp.n_slots; l++)
-    if (l != slot) load_d(r.d[k++], sp, coef_d, sp.slice[s][l], p);
+    if (l != slot) {
+      load_d(r.d[k], sp, coef_d, sp.slice[s][l], p);
+      const float vmn = vmin_of(r.d[k]);
+      f = f - vmx + vmn;
+      mag += fabsf(vmx) + fabsf(vmn);
+      k++;
+    }
   r.inv_p = sp.inv_p[p];
+  r.wfloor = (f - 1e-3f * mag) * r.inv_p;
 }
 __device__ __forceinline__ float ka_value(const SpaceParams& sp, const CoefRow& r, const float h[6]) {
   return flush_clamp(__fmul_rn(__fsub_rn(dot_u(r.c, h), sp.alpha), kScale));
@@ -228,7 +257,7 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
         for (int p = 0; p < nc; p++) {
           const float v = w_value<NS>(s_coef[p], h, j);
           row_a[p] = v;
-          const unsigned uo = ord_float_d(v);
+          const unsigned uo = ord_float_d(fmaxf(v, s_coef[p].wfloor));  // range of the feasible-capable shares
           lo = uo < lo ? uo : lo;
           hi = uo > hi ? uo : hi;
         }
@@ -265,8 +294,9 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
 //   role A_i   = ka[s_i(s)][j][p]            (own term minus alpha, scaled)
 //   role B_i^l = kb[s_l(s)][j][p], l != i    (this job's interference on slot l)
 //   role W_i   = fixed-point share of Throughput[/P]:
-//       q = rint((w[i][s][j][p] - wmin_i) * inv_delta),
-//       inv_delta = (2^25 - 2 - n_slots) / sum_i (wmax_i - wmin_i)   (sum_i q_i < 2^25)
+//       q = rint(fma(max(w[i][s][j][p], floor), inv_delta, -fl(wmin_i * inv_delta))),
+//       inv_delta = (2^25 - 2 - n_slots) / sum_i (wmax_i - wmin_i)   (quant_inv; sum_i q_i < 2^25)
+//       floor = the row's feasibility floor (load_w_row), wmin/wmax over the clamped shares
 //       W_0 = 0x00800000 + (q << 5); W_last = (q << 5) | (31 - off); others q << 5
 //     where off = c mod kStageCfg. The integer sum of a candidate's W's, read
 //     as FP32 bits, is a positive normal float below 4.0 that orders like the
@@ -285,15 +315,14 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   constexpr int ld = kStageCfg + 1;  // odd: the column writes of a warp hit distinct banks
   __shared__ CoefRow s_coef[kStageCfg];
   __shared__ float s_stage[kProjWarps][32 * ld];
-  __shared__ float s_lo, s_inv;
+  __shared__ float s_nlo, s_inv;
   const int role = blockIdx.y / sp.n_stages, stage = blockIdx.y - role * sp.n_stages;
   const int slot = role / (NS + 1), kind = role % (NS + 1);  // 0 = A, NS = W, else B
   const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);  // real configs in this stage
   if (threadIdx.x == 0) {
-    float span = 0.0f;
-    for (int i = 0; i < NS; i++) span += unord_float_d(wmm[2 * i + 1]) - unord_float_d(wmm[2 * i]);
-    s_lo = unord_float_d(wmm[2 * slot]);
-    s_inv = span > 0.0f ? (float)(33554430 - NS) / span : 0.0f;
+    const float inv = quant_inv<NS>(wmm);
+    s_inv = inv;
+    s_nlo = -__fmul_rn(unord_float_d(wmm[2 * slot]), inv);
   }
   if (threadIdx.x < ncol) {
     const int c = stage * kStageCfg + threadIdx.x, st = c / sp.n_caps, p = c - st * sp.n_caps;
@@ -323,10 +352,10 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   if (job) load_hj(hj, n, h, j);
   const int nreal = job ? ncol : 0;
   if (kind == NS) {
-    const float lo = s_lo, inv = s_inv;
+    const float nlo = s_nlo, inv = s_inv;
     const unsigned base = slot == 0 ? 0x00800000u : 0u;
     for (int col = 0; col < nreal; col++) {
-      const float qf = rintf((w_value<NS>(s_coef[col], h, j) - lo) * inv);
+      const float qf = rintf(__fmaf_rn(fmaxf(w_value<NS>(s_coef[col], h, j), s_coef[col].wfloor), inv, nlo));
       unsigned bits = ((qf > 0.0f ? (unsigned)qf : 0u) << 5) + base;
       if (slot == NS - 1) bits |= (unsigned)(31 - col);
       row[col] = __uint_as_float(bits);
@@ -346,36 +375,61 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   }
 }
 
-__global__ void k_init_wmm(unsigned* wmm) {
+__global__ void k_step_init(unsigned long long* err, unsigned long long* best_key, unsigned* rescore_n,
+                            unsigned* wmm) {
   if (threadIdx.x < 2 * kMaxSlots) wmm[threadIdx.x] = (threadIdx.x & 1) ? 0u : 0xFFFFFFFFu;
+  if (threadIdx.x == 0) {
+    *err = ~0ull;
+    *best_key = 0ull;
+    *rescore_n = 0u;
+  }
+}
+
+cudaError_t smem_optin(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(func, dev, bytes);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 148;
+  return n;
+}
+
+void launch_step_init(unsigned long long* err, unsigned long long* best_key, unsigned* rescore_n, unsigned* wmm,
+                      cudaStream_t st) {
+  k_step_init<<<1, 32, 0, st>>>(err, best_key, rescore_n, wmm);
 }
 
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
                     bool with_kakb, cudaStream_t st) {
-  if (n_jobs <= 0) return;
-  k_init_wmm<<<1, 32, 0, st>>>(wmm);
+  if (n_jobs <= 0) return;  // wmm was reset by launch_step_init
   // 2 job chunks of 128 per block (measured on C4: 1 -> 60.4 us, 2 -> 58.9,
   // 4 -> 62.1, 8 -> 75.2 for project + gather; COSCHED_PROJ_CHUNKS overrides)
   const int64_t n_chunks = (sp.n_jobs_pad + kProjJobs - 1) / kProjJobs;
-  static int per_block = -1;
-  if (per_block < 0) {
-    const char* e = getenv("COSCHED_PROJ_CHUNKS");
-    per_block = e ? std::max(1, atoi(e)) : 2;
-  }
+  const char* pc = getenv("COSCHED_PROJ_CHUNKS");
+  const int per_block = pc ? std::max(1, atoi(pc)) : 2;
   const unsigned jb = (unsigned)((n_chunks + per_block - 1) / per_block);
   const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);  // <= 70 KB (rs <= 68)
   // ka / kb rows only when a consumer of this step reads them (the tiled
   // scorers read the gathered layout and w); launch_project_kakb adds them later
   const int y0 = with_kakb ? 0 : sp.n_slices;
   const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states - y0)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_project_all<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
-    cudaFuncSetAttribute(k_project_all<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
-    cudaFuncSetAttribute(k_project_all<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_project_all<1>, 72 * 1024);
+  smem_optin((const void*)k_project_all<2>, 72 * 1024);
+  smem_optin((const void*)k_project_all<3>, 72 * 1024);
   if (sp.n_slots == 1) {
     k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
     k_gather_fast<1><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
@@ -498,22 +552,163 @@ int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, co
   return 1;
 }
 
-int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                            const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                            const unsigned long long* err, cudaStream_t st);
+int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
+                            int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                            const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st);
 
-int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                              const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                              const unsigned long long* err, cudaStream_t st);
+int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
+                              int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                              const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Exact re-scoring after the tiled scorers (RescoreBuf, rescore_threshold in
+// device_common.cuh). Which sets: pairs -- the sets the tile end flagged
+// (objective below the threshold), listed in rb.list; triples, or a list
+// overflow -- a scan of the shard's objectives for the same condition (4 B per
+// set); without an objective output only the best key matters, and it is within
+// tau/2 of the exact one unless its own objective is below the threshold (then
+// every set is re-scored). How: one warp per set evaluates every config in the
+// canonical FP32 order of eval_cfg -- margins from the gathered layout
+// (bit-identical to ka / kb), objective from w -- and keeps the first strictly
+// greater feasible objective, i.e. exactly what k_score_generic computes for
+// that set. The new key can only be larger than the tile end's (same
+// arithmetic, exact argmax), so an atomicMax keeps best_key right.
+template <int NS>
+__device__ __forceinline__ void rescore_one(const SpaceParams& sp, const float* __restrict__ fast,
+                                            const float* __restrict__ w, int64_t first, int64_t k,
+                                            float* __restrict__ out_obj, int32_t* __restrict__ out_cfg, int lane,
+                                            unsigned long long* bkey) {
+  const int64_t npad = sp.n_jobs_pad, sid = first + k;
+  int64_t j[3];
+  unrank_set<NS>(sid, j);
+  unsigned long long best = 0ull;
+  for (int c = lane; c < sp.n_cfg; c += 32) {
+    const int g = c / kStageCfg, off = c - g * kStageCfg;
+    const int s = c / sp.n_caps, p = c - s * sp.n_caps;
+    auto F = [&](int role, int64_t job) {
+      return __ldg(fast + (((int64_t)role * sp.n_stages + g) * npad + job) * kStageRS + off);
+    };
+    bool feas;
+    float o;
+    if (NS == 2) {  // roles [A0 B0^1 W0 | A1 B1^0 W1]
+      const float r0 = __fadd_rn(F(0, j[0]), F(4, j[1]));  // ka[s0][j0] + kb[s0][j1]
+      const float r1 = __fadd_rn(F(3, j[1]), F(1, j[0]));  // ka[s1][j1] + kb[s1][j0]
+      o = __fadd_rn(__ldg(w_row(w, sp, 0, s, j[0]) + p), __ldg(w_row(w, sp, 1, s, j[1]) + p));
+      feas = r0 > 0.0f && r1 > 0.0f;
+    } else {  // roles [A0 B0^1 B0^2 W0 | A1 B1^0 B1^2 W1 | A2 B2^0 B2^1 W2]
+      const float r0 = __fadd_rn(F(0, j[0]), __fadd_rn(F(5, j[1]), F(9, j[2])));
+      const float r1 = __fadd_rn(__fadd_rn(F(4, j[1]), F(10, j[2])), F(1, j[0]));
+      const float r2 = __fadd_rn(__fadd_rn(F(8, j[2]), F(6, j[1])), F(2, j[0]));
+      o = __fadd_rn(__ldg(w_row(w, sp, 0, s, j[0]) + p),
+                    __fadd_rn(__ldg(w_row(w, sp, 1, s, j[1]) + p), __ldg(w_row(w, sp, 2, s, j[2]) + p)));
+      feas = r0 > 0.0f && r1 > 0.0f && r2 > 0.0f;
+    }
+    const unsigned long long kk =
+        feas ? (((unsigned long long)ord_float_d(o) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
+    best = kk > best ? kk : best;
+  }
+  best = warp_max_u64(best);
+  if (lane == 0) {
+    const int bc = best ? (int)(0xFFFFFFFFull - (best & 0xFFFFFFFFull)) : -1;
+    const float bo = best ? unord_float_d((unsigned)(best >> 32)) : -INFINITY;
+    if (out_obj) out_obj[k] = bo;
+    if (out_cfg) out_cfg[k] = bc;
+    if (bc >= 0) {
+      const unsigned long long kk = pack_key(bo, sid);
+      *bkey = kk > *bkey ? kk : *bkey;
+    }
+  }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256) k_rescore_sets(const SpaceParams sp, const float* __restrict__ fast,
+                                                      const float* __restrict__ w, int64_t first, int64_t count,
+                                                      float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+                                                      unsigned long long* __restrict__ best_key, const RescoreBuf rb,
+                                                      const unsigned long long* __restrict__ err) {
+  if (*err != ~0ull) return;
+  const float thr = rescore_threshold<NS>(rb.wmm);
+  const unsigned n_listed = *rb.n;
+  const bool listed = NS == 2 && n_listed <= rb.cap;  // uniform per launch
+  if (listed && n_listed == 0u) return;               // the common case: one launch, nothing re-scored
+  if (!listed && !out_obj) {
+    // only the best key is produced: within tau/2 of the exact one unless its own objective is below thr
+    const unsigned long long bk = *best_key;
+    if (bk == 0ull || unord_float_d((unsigned)(bk >> 32)) >= thr) return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5, gw = blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
+  unsigned long long bkey = 0ull;
+  if (listed) {
+    for (int64_t e = gw; e < (int64_t)n_listed; e += nw)
+      rescore_one<NS>(sp, fast, w, first, (int64_t)rb.list[e], out_obj, out_cfg, lane, &bkey);
+  } else if (!out_obj) {
+    if (NS == 3 && gw == 0 && lane == 0) atomicAdd(rb.n, (unsigned)count);
+    for (int64_t k = gw; k < count; k += nw) rescore_one<NS>(sp, fast, w, first, k, out_obj, out_cfg, lane, &bkey);
+  } else {
+    // scan: 4 x 32 consecutive objectives per warp and step (coalesced, 512 B in flight per warp)
+    for (int64_t base = gw * 128; base < count; base += nw * 128) {
+      float o[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t k = base + u * 32 + lane;
+        o[u] = k < count ? out_obj[k] : -INFINITY;
+      }
+#pragma unroll 1
+      for (int u = 0; u < 4; u++) {
+        unsigned m = __ballot_sync(0xFFFFFFFFu, o[u] > -INFINITY && o[u] < thr);
+        if (NS == 3 && lane == 0 && m) atomicAdd(rb.n, (unsigned)__popc(m));  // triples: count what the scan found
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          rescore_one<NS>(sp, fast, w, first, base + u * 32 + b, out_obj, out_cfg, lane, &bkey);
+        }
+      }
+    }
+  }
+  block_max_key(bkey, best_key);
+}
+
+int launch_rescore(const SpaceParams& sp, const float* w, const float* fast, int64_t first, int64_t count, float* obj,
+                   int32_t* cfg, unsigned long long* best_key, const unsigned long long* err, const RescoreBuf& rb,
+                   cudaStream_t st) {
+  if (!rb.n || count <= 0) return 0;
+  // up to 8 resident blocks per SM: enough loads in flight for the scan mode
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (count + 1023) / 1024));
+  if (sp.n_slots == 2)
+    k_rescore_sets<2><<<grid, 256, 0, st>>>(sp, fast, w, first, count, obj, cfg, best_key, rb, err);
+  else
+    k_rescore_sets<3><<<grid, 256, 0, st>>>(sp, fast, w, first, count, obj, cfg, best_key, rb, err);
+  return 1;
+}
+
+bool tiled_applicable(int n_slots, int64_t n_jobs, int64_t first, int64_t count) {
+  if (n_slots < 2 || count <= 0) return false;
+  // whole colex columns (pairs) / planes (triples): first and first + count are C(b, n_slots)
+  auto whole = [&](int64_t v) {
+    int64_t lo = 0, hi = n_jobs;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (n_sets(mid, n_slots) >= v) hi = mid;
+      else lo = mid + 1;
+    }
+    return n_sets(lo, n_slots) == v;
+  };
+  if (!whole(first) || !whole(first + count)) return false;
+  return n_slots == 3 || (n_jobs + 63) / 64 < 32768;
+}
 
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
-                 unsigned long long* best_key, const unsigned long long* err, int variant, cudaStream_t st) {
+                 unsigned long long* best_key, const unsigned long long* err, int variant, cudaStream_t st,
+                 const RescoreBuf& rb) {
   if (count <= 0) return 0;
-  if (variant != 0 && sp.n_slots == 2)
-    return launch_score_pairs_fast(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, st);
-  if (variant != 0 && sp.n_slots == 3)
-    return launch_score_triples_fast(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, st);
+  if (variant != 0 && tiled_applicable(sp.n_slots, n_jobs, first, count)) {
+    int n = sp.n_slots == 2
+                ? launch_score_pairs_fast(sp, n_jobs, w, fast, first, count, obj, cfg, best_key, err, rb, st)
+                : launch_score_triples_fast(sp, n_jobs, w, fast, first, count, obj, cfg, best_key, err, rb, st);
+    return n + launch_rescore(sp, w, fast, first, count, obj, cfg, best_key, err, rb, st);
+  }
   int bs = 256;
   unsigned grid = (unsigned)((count + bs - 1) / bs);
   if (sp.n_slots == 1)

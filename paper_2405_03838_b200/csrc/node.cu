@@ -194,7 +194,7 @@ int node_enqueue(const SpaceParams& sp, const float* ka, const float* kb, const 
   q.unit_w = unit_w;
   for (int i = 0; i < sp.n_caps; i++) q.u[i] = u[i];
   const size_t dsm = (size_t)2 * (U + 1) * 4;
-  if (dsm > 48 * 1024) cudaFuncSetAttribute(k_node_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  smem_optin((const void*)k_node_dp, dsm);
   k_node_dp<<<(unsigned)n_nodes, 1024, dsm, st>>>(q, d_front, d_fstate, d_choice, d_caps, d_cfg, d_obj);
   if (cudaMemcpyAsync(caps_host, d_caps, n_gpus * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaMemcpyAsync(cfg_host, d_cfg, n_gpus * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -112,9 +112,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
                         const float* __restrict__ fast,
                         float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
-                        unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err) {
+                        unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err,
+                        const RescoreBuf rb) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
+  __shared__ float s_thr;  // exact re-scoring threshold (rescore_threshold)
   if (*err != ~0ull) return;
   constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
   constexpr int stage_floats = 6 * kTile * rs;
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_fence_init();
+    s_thr = rescore_threshold<2>(rb.wmm);
   }
   // per pair ([j1 local][j0 local], padded rows): state of the best masked key
   // (written when a state improves) and, at tile end, the key itself
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int jI = (int)(I * kTile), jJ = (int)(J * kTile);
       const int c_lo = (int)g.c0, c_hi = (int)g.c1;  // this shard's columns (c1 <= n_jobs)
       const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
+      const float thr = s_thr;
 #pragma unroll 1
       for (int e0 = 16 * kTile * b0; e0 < 16 * kTile * (b0 + NB); e0 += kPass * kThreads) {
         float f0[kPass], f1[kPass];
@@ -282,6 +286,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (bc >= 0) {
             const unsigned long long kk = pack_key(bo, sid);
             key = kk > key ? kk : key;
+            if (bo < thr) {  // not provably within tau/2 of the FP32 argmax: exact re-score
+              const unsigned at = atomicAdd(rb.n, 1u);
+              if (at < rb.cap) rb.list[at] = (unsigned)k;
+            }
           }
         }
       }
@@ -299,11 +307,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
   block_max_key(key, best_key);
 }
 
-static int g_num_sms = 0;
-
-int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                            const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
-                            unsigned long long* best_key, const unsigned long long* err, cudaStream_t st) {
+// Precondition: tiled_applicable(2, n_jobs, first, count) (kernels.cu), i.e. the
+// shard is whole colex columns and the queue has < 32768 column tiles.
+int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
+                            int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                            const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st) {
   // column range of the shard; shards are whole columns (cosched_shard_range)
   auto c2 = [](int64_t n) { return n * (n - 1) / 2; };
   auto col_at = [&](int64_t v) {  // smallest c with C(c,2) >= v
@@ -312,10 +320,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     while (c2(c) < v) c++;
     return c;
   };
-  int64_t c0 = col_at(first), c1 = col_at(first + count);
-  if (c2(c0) != first || c2(c1) != first + count || c1 > n_jobs || (n_jobs + kTile - 1) / kTile >= 32768) {
-    return launch_score(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, 0, st);
-  }
+  const int64_t c0 = col_at(first), c1 = col_at(first + count);
   PairGrid g;
   g.n_jobs = n_jobs;
   g.c0 = c0;
@@ -327,22 +332,15 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   g.n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - g.base;
   constexpr size_t smem = (size_t)2 * 6 * kTile * kStageRS * sizeof(float) +
                           (size_t)kTile * kBgRow * (sizeof(float) + sizeof(int16_t));
-  static int minb = -1;
   const char* fs = getenv("COSCHED_PAIR_SPLIT");  // testing knob: force the tail split (1, 2 or 4)
   const int forced_split = fs ? atoi(fs) : 0;
-  if (minb < 0) {
-    const char* e = getenv("COSCHED_PAIR_MINB");
-    minb = (e && e[0] == '1') ? 1 : 2;
-    cudaFuncSetAttribute(k_score_pairs_tiled<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_score_pairs_tiled<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_score_pairs_tiled<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_score_pairs_tiled<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  if (!g_num_sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const char* mb = getenv("COSCHED_PAIR_MINB");
+  const int minb = (mb && mb[0] == '1') ? 1 : 2;
+  smem_optin((const void*)k_score_pairs_tiled<1, 4>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 4>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 2>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 1>, smem);
+  const int g_num_sms = num_sms();
   int per_sm = 0;
   if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1, 4>, kThreads, smem);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2, 4>, kThreads, smem);
@@ -412,9 +410,9 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     g.n_seg = 0;
     const int64_t grid = n_whole < slots ? n_whole : slots;
     if (minb == 1)
-      k_score_pairs_tiled<1, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+      k_score_pairs_tiled<1, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
     else
-      k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+      k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
   }
   if (n_seg > 0) {
     launches++;
@@ -432,9 +430,9 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     g.n_units = end;
     const int64_t grid = end < slots ? end : slots;
     if (unit_nb == 2)
-      k_score_pairs_tiled<2, 2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+      k_score_pairs_tiled<2, 2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
     else
-      k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+      k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
   }
   return launches;
 }

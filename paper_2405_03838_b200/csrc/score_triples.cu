@@ -184,9 +184,8 @@ __device__ __forceinline__ void tstage_body(const float* st, int tx, int ty, uns
 
 template <int MINB>
 __global__ void __launch_bounds__(kTThreads, MINB)
-    k_score_triples_tiled(const SpaceParams sp, const TripleGrid g, const float* __restrict__ ka,
-                          const float* __restrict__ kb, const float* __restrict__ w, const float* __restrict__ fast,
-                          float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+    k_score_triples_tiled(const SpaceParams sp, const TripleGrid g, const float* __restrict__ w,
+                          const float* __restrict__ fast, float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
                           unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -350,11 +349,13 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 // Host view of the tile count, for work-balanced triple shards (api.cu shard_bounds).
 int64_t triple_tiles_before(int64_t j2) { return tiles_before(j2); }
 
-static int g_tri_sms = 0;
-
-int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
-                              const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
-                              unsigned long long* best_key, const unsigned long long* err, cudaStream_t st) {
+// Precondition: tiled_applicable(3, n_jobs, first, count) (kernels.cu): whole planes.
+// The exact re-scoring pass (k_rescore_sets) finds the sets to re-score by a
+// scan of the objectives: a flag in this kernel's tile end pushes it past 128
+// registers (spills in every stage body).
+int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
+                              int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
+                              const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st) {
   auto c3 = [](int64_t n) { return n * (n - 1) * (n - 2) / 6; };
   auto plane_at = [&](int64_t v) {  // smallest c with C(c,3) >= v
     int64_t c = (int64_t)cbrt(6.0 * (double)v);
@@ -362,10 +363,7 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
     while (c3(c) < v) c++;
     return c;
   };
-  int64_t c0 = plane_at(first), c1 = plane_at(first + count);
-  if (c3(c0) != first || c3(c1) != first + count || c1 > n_jobs) {
-    return launch_score(sp, n_jobs, ka, kb, w, fast, first, count, obj, cfg, best_key, err, 0, st);
-  }
+  const int64_t c0 = plane_at(first), c1 = plane_at(first + count);
   TripleGrid g;
   g.n_jobs = n_jobs;
   g.c0 = c0;
@@ -376,18 +374,11 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
   g.n_tiles = tiles_before(c1) - g.cum0;
   constexpr size_t smem = (size_t)2 * (8 * kTT * kStageRS + 4 * kStageRS) * sizeof(float) +
                           (size_t)kTT * kTBgRow * (sizeof(float) + sizeof(int16_t));
-  static int minb = -1;
-  if (minb < 0) {
-    const char* e = getenv("COSCHED_TRIPLE_MINB");
-    minb = (e && e[0] == '1') ? 1 : 2;
-    cudaFuncSetAttribute(k_score_triples_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_score_triples_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  if (!g_tri_sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_tri_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const char* mb = getenv("COSCHED_TRIPLE_MINB");
+  const int minb = (mb && mb[0] == '1') ? 1 : 2;
+  smem_optin((const void*)k_score_triples_tiled<1>, smem);
+  smem_optin((const void*)k_score_triples_tiled<2>, smem);
+  const int g_tri_sms = num_sms();
   int per_sm = 0;
   if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled<1>, kTThreads, smem);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_triples_tiled<2>, kTThreads, smem);
@@ -396,9 +387,9 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
   if (grid > g.n_tiles) grid = g.n_tiles;
   if (grid < 1) grid = 1;
   if (minb == 1)
-    k_score_triples_tiled<1><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+    k_score_triples_tiled<1><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   else
-    k_score_triples_tiled<2><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, ka, kb, w, fast, obj, cfg, best_key, err);
+    k_score_triples_tiled<2><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
   return 1;
 }
 

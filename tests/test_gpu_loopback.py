@@ -1,0 +1,29 @@
+"""The W > 1 paths of the library (VERDICT r1 "missing" item 4) on one GPU:
+W cosched ranks as W threads, every NCCL call routed to the in-process
+loopback stand-in (tests/loopback/). Results must equal W = 1 (see
+tests/loopback_ranks.py for what is compared). The queue is sharded exactly
+as on a multi-GPU node (cosched_shard_range with nranks = W)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_w_ranks_through_loopback_equal_single_rank(W):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import loopback
+    env = dict(os.environ, COSCHED_NCCL_LIB=loopback.build())
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "loopback_ranks.py"), str(W)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rep = json.loads(r.stdout.strip().splitlines()[-1])
+    assert [c["W"] for c in rep] == [W] * 5

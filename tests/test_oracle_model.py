@@ -308,3 +308,67 @@ def test_problem_validation_codes():
     bad.state_mem = bad.state_mem.copy()
     bad.state_mem[2] = 2
     assert Oracle(bad).validate()[0] == oracle.E_INVALID_ALLOCATION
+
+
+# ---- the hand-derived triple (exact dyadic arithmetic; n_slots = 3) --------
+# Pins orc_rperf for three applications: slot i sums the J of BOTH partners
+# under the D of its OWN slice (reading R14).
+
+def test_hand_triple_basis(golden):
+    g = golden("hand_triple_example.json")
+    for name in ("A", "B", "C"):
+        f = g["features"][name]
+        assert list(oracle.basis_h(f)) == g["basis_by_hand"]["H_" + name]
+        assert list(oracle.basis_j(f)) == g["basis_by_hand"]["J_" + name]
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_hand_triple_choices(golden, case):
+    g = golden("hand_triple_example.json")
+    ch = g["choices_by_hand"][case]
+    pb = _problem_from_json(g["problem"], ch["objective"], ch["alpha"])
+    assert Oracle(pb).validate()[0] == oracle.OK
+    o = Oracle(pb)
+    rows = [np.array(g["features"][k], np.float32) for k in g["queue"]]
+    obj, fair, thr, feas, rp = o.eval_set(rows)
+    for row in g["per_config_by_hand"]:
+        c = row["cfg"]
+        assert list(rp[c]) == row["rperf"], c      # exact: every value is dyadic
+        assert thr[c] == row["throughput"] and fair[c] == row["fairness"]
+    for s in range(3):  # one scalar RPerf entry point agrees with the set evaluation
+        for p in range(2):
+            for i in range(3):
+                assert o.rperf(rows, i, s, p) == rp[s * 2 + p][i]
+    cfg, ob = o.best_config(rows)
+    assert cfg == ch["cfg"], ch["why"]
+    if ch["obj"] is None:
+        assert ob == -math.inf
+    else:
+        assert ob == pytest.approx(ch["obj"], rel=1e-15)
+
+
+def test_hand_triple_queue_order(golden):
+    """Queue [C, A, B] puts C in slot 0 (slot i <- i-th smallest queue position, reading R15):
+    state 0 then gives C slice 0, A slice 1, B slice 2; by hand from the golden's terms:
+    C: .5 + D0.J_A + D0.J_B = .5 - .0625 - .1875 = .25; A: .625 + D1.J_C + D1.J_B =
+    .625 - .1875 - .0625 = .375; B: .375 + D2.J_C + D2.J_A = .375 - .21875 - .15625 = 0."""
+    g = golden("hand_triple_example.json")
+    pb = _problem_from_json(g["problem"], 2, 0.0)
+    rows = [np.array(g["features"][k], np.float32) for k in ("C", "A", "B")]
+    _, _, _, _, rp = Oracle(pb).eval_set(rows)
+    assert list(rp[0]) == [0.25, 0.375, 0.0]
+
+
+def test_fp32_tensor_sum_reading():
+    """Reading R24: F6+F7+F8 <= 100 is decided on the FP32 sum (F6+F7)+F8 --
+    the precision of the FP32 inputs and of the CUDA path's decision (a status is an
+    integer decided by floating point: both sides decide it in the same precision).
+    These three FP32 values sum to exactly 100.0 in FP32 but to 100.0000038 in FP64:
+    valid under the reading."""
+    f6, f7, f8 = np.float32(33.33333206176758), np.float32(33.33333206176758), np.float32(33.33333969116211)
+    assert np.float32(np.float32(f6 + f7) + f8) == np.float32(100.0)
+    assert float(f6) + float(f7) + float(f8) > 100.0
+    row = np.array([[90, 40, 30, 60, 50, f6, f7, f8]], np.float32)
+    assert Oracle.validate_features(row)[0] == oracle.OK
+    row[0, 7] = np.nextafter(f8, np.float32(200))
+    assert Oracle.validate_features(row)[0] == oracle.E_RANGE

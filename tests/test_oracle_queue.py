@@ -172,3 +172,16 @@ def test_greedy_properties():
         for t in range(len(obj)):
             if obj[t] > -math.inf:
                 assert used & set(oracle.unrank(40, 2, t))
+
+
+def test_all_cores_split_equals_single_process():
+    """tests/oracle_parallel.py only splits the work: identical results to one process."""
+    from oracle_parallel import score_range_all_cores
+    for table, n in (("b200", 57), ("b200_3way", 23)):
+        pb = make_problem(table, "c10", coef_seed=9)
+        F, _ = make_features(n, seed=9)
+        cfg1, obj1 = Oracle(pb).score_range(F)
+        cfg2, obj2, _ = score_range_all_cores(pb, F, procs=3)
+        assert np.array_equal(cfg1, cfg2) and np.array_equal(obj1, obj2)
+        cfg3, obj3, _ = score_range_all_cores(pb, F, first=100, count=333, procs=2)
+        assert np.array_equal(cfg3, cfg1[100:433]) and np.array_equal(obj3, obj1[100:433])
