@@ -136,11 +136,15 @@ cosched_status cosched_set_comm(cosched_t h, const void* nccl_unique_id, int ran
 cosched_status cosched_set_shard_view(cosched_t h, int rank, int nranks);
 
 /* This rank's set range for a queue of n_jobs (host only, no CUDA). Rank r of
- * W gets the sets whose largest position lies in [b_r, b_{r+1}). Pairs (and
- * solo): b_r is the smallest b with C(b, n_slots) >= r * C(n_jobs, n_slots) / W
- * (balanced on sets). Triples: balanced on the triple scorer's work instead,
- * b_r the smallest b with T(b) >= r * T(n_jobs) / W, where T(b) = sum over
- * planes 1 <= j < b of t(t+1)/2 with t = ceil(j / 64) (its 64 x 64 tiles). */
+ * W gets the sets whose largest position lies in [b_r, b_{r+1}). Pairs: the
+ * b_r are multiples of 64 (whole column blocks of the pair scorer's 64 x 64
+ * tiles) chosen by a DP that minimises the largest modelled scorer time of a
+ * rank on a B200 (whole-tile rounds on 296 CTA slots plus the stage-split last
+ * round; api.cu pair_block_bounds); a rank may get no sets when n_jobs is
+ * small. Solo: b_r the smallest b with b >= r * n_jobs / W. Triples: balanced
+ * on the triple scorer's tiles, b_r the smallest b with T(b) >= r * T(n_jobs) / W,
+ * where T(b) = sum over planes 1 <= j < b of t(t+1)/2 with t = ceil(j / 64).
+ * A pure function of (n_jobs, n_slots, rank, W): identical on every rank. */
 cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets);
 
 /* The same partition without a handle (host only): rank of nranks, sets of n_slots jobs. */

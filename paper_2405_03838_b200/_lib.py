@@ -10,7 +10,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libcosched.so")
+# COSCHED_LIB_PATH: an alternative build of the same library (compile-time
+# variants for A/B timing, tools/build_variants.py); the default is the in-tree build
+SO_PATH = os.environ.get("COSCHED_LIB_PATH") or os.path.join(HERE, "libcosched.so")
 
 STATUS = {0: "OK", 2: "INFEASIBLE", 10: "E_ARG", 11: "E_INVALID_ALLOCATION", 12: "E_UNKNOWN_KEY",
           13: "E_DEGENERATE_PROFILE", 14: "E_RANGE", 15: "E_STATE", 20: "E_CUDA", 21: "E_NCCL", 22: "E_OOM"}

@@ -12,6 +12,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -119,6 +121,8 @@ struct cosched_ctx {
   int view_nranks = 1;  // shard view without comm (tests)
   int64_t greedy_rounds = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t side = nullptr;                 // partial-column units of the pair scorer (PairMerge)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host copies of the table (ground-truth evaluation)
   std::vector<int32_t> h_gpcs, h_mem;
   std::vector<float> h_caps;
@@ -151,6 +155,100 @@ float unord_float(uint32_t o) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+}  // namespace cosched
+// Pair shards: whole 64-column blocks of the triangle (the pair scorer's tile
+// columns; no shard boundary inside a block, so no partial-column units except
+// the queue's ragged last block), chosen by a DP over block boundaries that
+// minimises the largest modelled scorer time. The model, in
+// rounds of the persistent launch on a B200 (148 SMs x 2 CTAs = 296 slots):
+// a rank's whole tiles take floor(tiles / 296) rounds, its last partial round
+// of R tiles is split into q stage groups (score_pairs.cu) costing
+// ceil(R q / 296) x (ceil(16 / q) + 0.3 [q > 1]) / 16 rounds, and the ragged
+// last block's single-row-group units 0.47 of a tile each. A pure function of
+// (n_jobs, nranks), identical on every rank; cached.
+static const std::vector<int64_t>& pair_block_bounds(int64_t n_jobs, int nranks) {
+  static std::mutex mu;
+  static std::map<std::pair<int64_t, int>, std::vector<int64_t>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({n_jobs, nranks});
+  if (it != cache.end()) return it->second;
+  constexpr double kSlots = 296.0, kStages = 16.0, kUnit = 0.3, kPartial = 0.47;
+  const int64_t nb = (n_jobs + 63) / 64;
+  auto tail = [&](int64_t R) {
+    if (R <= 0) return 0.0;
+    double best = 1e30;
+    for (int q = 1; q <= (int)kStages; q++) {
+      const double len = std::ceil(R * q / kSlots) * (std::ceil(kStages / q) + (q > 1 ? kUnit : 0.0)) / kStages;
+      best = std::min(best, len);
+    }
+    return best;
+  };
+  auto rank_time = [&](int64_t B0, int64_t B1) {
+    const int64_t tiles = B1 * (B1 + 1) / 2 - B0 * (B0 + 1) / 2;
+    const int64_t part = (B1 == nb && n_jobs % 64) ? B1 : 0;  // the ragged block's tiles (as units)
+    const int64_t full = tiles - part, rounds = full > (int64_t)kSlots ? full / (int64_t)kSlots : 0;
+    return (double)rounds + tail(full - rounds * (int64_t)kSlots) + part * kPartial / kSlots;
+  };
+  std::vector<int64_t> b(nranks + 1, 0);
+  if (nranks == 1 || nb <= 1) {
+    for (int r = 1; r <= nranks; r++) b[r] = nb;
+  } else {
+    // best[r][B]: smallest max time of blocks [0, B) over r ranks (rank order = block order)
+    std::vector<std::vector<double>> best(nranks + 1, std::vector<double>(nb + 1, 1e300));
+    std::vector<std::vector<int64_t>> arg(nranks + 1, std::vector<int64_t>(nb + 1, 0));
+    best[0][0] = 0.0;
+    for (int r = 1; r <= nranks; r++)
+      for (int64_t B = 0; B <= nb; B++)
+        for (int64_t P = 0; P <= B; P++) {
+          if (best[r - 1][P] >= 1e300) continue;
+          const double v = std::max(best[r - 1][P], rank_time(P, B));
+          if (v < best[r][B] - 1e-12) {
+            best[r][B] = v;
+            arg[r][B] = P;
+          }
+        }
+    b[nranks] = nb;
+    for (int r = nranks; r > 0; r--) b[r - 1] = arg[r][b[r]];
+  }
+  for (auto& x : b) x = std::min<int64_t>(64 * x, n_jobs);
+  return cache.emplace(std::make_pair(n_jobs, nranks), std::move(b)).first->second;
+}
+
+// Contiguous whole-column shards. Pairs: pair_block_bounds. Triples: balanced
+// on the triple scorer's tiles (its time per plane follows the tile count, the
+// small planes' diagonal and ragged tiles included), b_r the smallest b with
+// tiles_before(b) >= ceil(r * tiles_before(n_jobs) / W). Solo: balanced on sets.
+static void shard_bounds(int64_t n_jobs, int k, int rank, int nranks, int64_t* first, int64_t* count) {
+  if (k == 2) {
+    const std::vector<int64_t>& b = pair_block_bounds(n_jobs, nranks);
+    *first = cosched::n_sets(b[rank], 2);
+    *count = cosched::n_sets(b[rank + 1], 2) - *first;
+    return;
+  }
+  auto cost = [&](int64_t b) -> int64_t {
+    return k == 3 ? cosched::triple_tiles_before(b) : cosched::n_sets(b, k);
+  };
+  const int64_t total = cost(n_jobs);
+  auto boundary = [&](int r) -> int64_t {  // smallest b with cost(b) >= ceil(r * total / W)
+    if (r <= 0) return 0;
+    if (r >= nranks) return n_jobs;
+    __int128 num = (__int128)r * total;
+    int64_t target = (int64_t)((num + nranks - 1) / nranks);
+    int64_t lo = 0, hi = n_jobs;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (cost(mid) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  };
+  int64_t b0 = boundary(rank), b1 = boundary(rank + 1);
+  *first = cosched::n_sets(b0, k);
+  *count = cosched::n_sets(b1, k) - *first;
+}
+
+namespace cosched {
+
 int64_t pad_jobs(int64_t n_jobs) { return (n_jobs + 63) / 64 * 64; }
 
 size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_local, int nranks, char* base,
@@ -177,16 +275,26 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.job_key = (unsigned long long*)take((size_t)n_jobs * 8);
   w.taken = (uint32_t*)take((size_t)n_jobs * 4);
   w.picked = (unsigned long long*)take((size_t)n_jobs * 8 + 8);
-  w.alive = (int64_t*)take((size_t)n_sets_local * 8 + 8);
-  w.alive2 = (int64_t*)take((size_t)n_sets_local * 8 + 8);
+  // largest shard of any rank (the greedy's all-gathered batches are padded to it)
+  int64_t largest = n_sets_local;
+  for (int r = 0; r < nranks; r++) {
+    int64_t f, c;
+    shard_bounds(n_jobs, n_slots, r, nranks, &f, &c);
+    largest = std::max(largest, c);
+  }
+  w.alive = (int64_t*)take((size_t)largest * 8 + 8);
+  w.alive2 = (int64_t*)take((size_t)largest * 8 + 8);
   w.hist = (unsigned*)take((size_t)kHistBins * 4);
   w.mm = (unsigned*)take(16);
-  // nranks = 0: no communicator; else the greedy all-gathers per-rank batches
+  // nranks = 0: no communicator; else the greedy all-gathers per-rank batches.
+  // The per-rank batch capacity must be the same on every rank (the switch to
+  // the fallback rounds is taken by all ranks or none): it is bounded by the
+  // largest shard of any rank, which every rank computes alike.
   // COSCHED_GREEDY_BATCH_CAP (testing knob): a smaller per-rank batch capacity, which
   // forces the locally-dominant-rounds fallback of the multi-rank greedy
   int64_t cap_max = (int64_t)16 << 20;
   if (const char* e = getenv("COSCHED_GREEDY_BATCH_CAP")) cap_max = std::max<int64_t>(1, atoll(e));
-  const int64_t cap = nranks > 0 ? std::min<int64_t>(n_sets_local, cap_max) : n_sets_local;
+  const int64_t cap = nranks > 0 ? std::min<int64_t>(largest, cap_max) : n_sets_local;
   w.batch_cap = cap;
   const int64_t gathered = nranks > 0 ? cap * nranks : 0;
   w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);
@@ -201,6 +309,10 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   if (const char* e = getenv("COSCHED_RESCORE_CAP")) rcap = std::max<int64_t>(0, atoll(e));  // testing knob: overflow path
   w.rescore_cap = (unsigned)std::min<int64_t>(std::max<int64_t>(n_sets_local, 1), rcap);
   w.rescore_list = (unsigned*)take((size_t)std::max<unsigned>(w.rescore_cap, 1u) * 4);
+  // the pair scorer's stage-split tail: at most one CTA-slot round of tiles
+  // (2 resident CTAs per SM), 32 KB each (pairs only)
+  w.merge_tiles = n_slots == 2 ? 2 * (int64_t)num_sms() : 0;
+  w.merge = (unsigned long long*)take((size_t)w.merge_tiles * 64 * 64 * 8);
   w.rescore_n = (unsigned*)take(8);
   w.bytes = off;
   if (ws) *ws = w;
@@ -361,6 +473,9 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
             cudaMallocHost(&h->h_pinned, 8 * 8) == cudaSuccess && cudaMalloc(&h->d_sums, 4 * 8) == cudaSuccess &&
             cudaEventCreate(&h->ev[0]) == cudaSuccess && cudaEventCreate(&h->ev[1]) == cudaSuccess &&
             cudaEventCreate(&h->ev[2]) == cudaSuccess && cudaEventCreate(&h->ev[3]) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_c, d->coef_c, nc * 6 * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_d, d->coef_d, nc * 3 * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) {
@@ -389,6 +504,9 @@ void cosched_destroy(cosched_t h) {
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
     for (int i = 0; i < 4; i++)
       if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->side) cudaStreamDestroy(h->side);
   }
   delete h;
 }
@@ -476,34 +594,6 @@ void cosched_unpack_key(uint64_t key, float* obj, int64_t* set_id) {
   }
   if (obj) *obj = unord_float((uint32_t)(key >> 32));
   if (set_id) *set_id = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
-}
-
-// Contiguous whole-column shards. Pairs: balanced on sets, b_r the smallest b
-// with C(b,2) >= ceil(r * total / W). Triples: balanced on the triple scorer's
-// tiles (its time per plane follows the tile count, the small planes' diagonal
-// and ragged tiles included), b_r the smallest b with tiles_before(b) >=
-// ceil(r * tiles_before(n_jobs) / W).
-static void shard_bounds(int64_t n_jobs, int k, int rank, int nranks, int64_t* first, int64_t* count) {
-  auto cost = [&](int64_t b) -> int64_t {
-    return k == 3 ? cosched::triple_tiles_before(b) : cosched::n_sets(b, k);
-  };
-  const int64_t total = cost(n_jobs);
-  auto boundary = [&](int r) -> int64_t {  // smallest b with cost(b) >= ceil(r * total / W)
-    if (r <= 0) return 0;
-    if (r >= nranks) return n_jobs;
-    __int128 num = (__int128)r * total;
-    int64_t target = (int64_t)((num + nranks - 1) / nranks);
-    int64_t lo = 0, hi = n_jobs;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) / 2;
-      if (cost(mid) >= target) hi = mid;
-      else lo = mid + 1;
-    }
-    return lo;
-  };
-  int64_t b0 = boundary(rank), b1 = boundary(rank + 1);
-  *first = cosched::n_sets(b0, k);
-  *count = cosched::n_sets(b1, k) - *first;
 }
 
 cosched_status cosched_shard_range(cosched_t h, int64_t n_jobs, int64_t* first_set, int64_t* n_sets_out) {
@@ -681,8 +771,14 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     rb.list = ws.rescore_list;
     rb.n = ws.rescore_n;
     rb.cap = ws.rescore_cap;
+    PairMerge pm;
+    pm.buf = ws.merge;
+    pm.tiles = ws.merge_tiles;
+    pm.side = h->side;
+    pm.ev_fork = h->ev_fork;
+    pm.ev_join = h->ev_join;
     h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
-                                ws.err, h->variant, st, rb);
+                                ws.err, h->variant, st, rb, pm);
   }
   cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();

@@ -70,6 +70,18 @@ struct RescoreBuf {
   unsigned cap = 0;
 };
 
+// Merge buffer of the pair scorer's stage-split tail (score_pairs.cu): one u64
+// per pair of up to `tiles` 64 x 64 tiles.
+struct PairMerge {
+  unsigned long long* buf = nullptr;
+  int64_t tiles = 0;
+  // the handle's side stream: the partial-column units run on it concurrently
+  // with the whole-tile and stage-split launches (forked after the gather,
+  // joined before the re-scoring pass); null = everything on the caller's stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+
 // Device-side tables owned by a handle.
 struct DeviceTables {
   float* coef_c = nullptr;  // [n_caps][n_slices][6]
@@ -103,6 +115,8 @@ struct Workspace {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   int64_t batch_cap = 0;                   // keys per rank per greedy batch
+  unsigned long long* merge = nullptr;     // [merge_tiles][64 * 64] (PairMerge)
+  int64_t merge_tiles = 0;
   unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
   unsigned* rescore_n = nullptr;           // [1]
   unsigned rescore_cap = 0;
@@ -171,7 +185,8 @@ int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, co
 // flagged sets (rb), when tiled_applicable(), else the generic kernel.
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                 const unsigned long long* err, int variant, cudaStream_t st, const RescoreBuf& rb = RescoreBuf());
+                 const unsigned long long* err, int variant, cudaStream_t st, const RescoreBuf& rb = RescoreBuf(),
+                 const PairMerge& merge = PairMerge());
 // Whether the tiled scorer takes shard [first, first + count) of an n_jobs queue
 // (whole colex columns / planes; pair queues below 32768 column tiles). The one
 // place the tiled-or-generic decision is made: score_all projects ka / kb for

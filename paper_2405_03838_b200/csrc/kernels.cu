@@ -554,7 +554,8 @@ int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, co
 
 int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
                             int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                            const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st);
+                            const unsigned long long* err, const RescoreBuf& rb, const PairMerge& merge,
+                            cudaStream_t st);
 
 int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
                               int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
@@ -701,11 +702,11 @@ bool tiled_applicable(int n_slots, int64_t n_jobs, int64_t first, int64_t count)
 int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                  const float* fast, int64_t first, int64_t count, float* obj, int32_t* cfg,
                  unsigned long long* best_key, const unsigned long long* err, int variant, cudaStream_t st,
-                 const RescoreBuf& rb) {
+                 const RescoreBuf& rb, const PairMerge& merge) {
   if (count <= 0) return 0;
   if (variant != 0 && tiled_applicable(sp.n_slots, n_jobs, first, count)) {
     int n = sp.n_slots == 2
-                ? launch_score_pairs_fast(sp, n_jobs, w, fast, first, count, obj, cfg, best_key, err, rb, st)
+                ? launch_score_pairs_fast(sp, n_jobs, w, fast, first, count, obj, cfg, best_key, err, rb, merge, st)
                 : launch_score_triples_fast(sp, n_jobs, w, fast, first, count, obj, cfg, best_key, err, rb, st);
     return n + launch_rescore(sp, w, fast, first, count, obj, cfg, best_key, err, rb, st);
   }
@@ -734,12 +735,18 @@ int launch_score(const SpaceParams& sp, int64_t n_jobs, const float* ka, const f
 // same FP32 values in the same canonical order, for steps whose projection
 // skipped the ka / kb rows (launch_project with_kakb = false).
 template <int NS>
-__device__ __forceinline__ void eval_cfg_hj(const SpaceParams& sp, const float* __restrict__ hj,
+__device__ __forceinline__ void eval_cfg_hj(const SpaceParams& sp, const float* __restrict__ s_hj,
                                             const float* __restrict__ coef_c, const float* __restrict__ coef_d,
-                                            const int64_t* j, int s, int p, float* r, float* o) {
+                                            int s, int p, float* r, float* o) {
+  // s_hj: the set's basis rows, slot i at s_hj + 12 i (shared memory)
   float h[NS][6], jv[NS][3];
 #pragma unroll
-  for (int i = 0; i < NS; i++) load_hj(hj, j[i], h[i], jv[i]);
+  for (int i = 0; i < NS; i++) {
+#pragma unroll
+    for (int t = 0; t < 6; t++) h[i][t] = s_hj[12 * i + t];
+#pragma unroll
+    for (int t = 0; t < 3; t++) jv[i][t] = s_hj[12 * i + 6 + t];
+  }
   auto KA = [&](int slot_of_slice, int i) {
     CoefRow cr;
     load_c(cr, sp, coef_c, sp.slice[s][slot_of_slice], p);
@@ -773,13 +780,13 @@ __device__ __forceinline__ void eval_cfg_hj(const SpaceParams& sp, const float* 
 template <bool HJ>
 __device__ __forceinline__ void eval_any(const SpaceParams& sp, const float* __restrict__ ka,
                                          const float* __restrict__ kb, const float* __restrict__ w,
-                                         const float* __restrict__ hj, const float* __restrict__ coef_c,
+                                         const float* __restrict__ s_hj, const float* __restrict__ coef_c,
                                          const float* __restrict__ coef_d, const int64_t* j, int s, int p, float* r,
                                          float* u) {
   if (HJ) {
-    if (sp.n_slots == 1) eval_cfg_hj<1>(sp, hj, coef_c, coef_d, j, s, p, r, u);
-    else if (sp.n_slots == 2) eval_cfg_hj<2>(sp, hj, coef_c, coef_d, j, s, p, r, u);
-    else eval_cfg_hj<3>(sp, hj, coef_c, coef_d, j, s, p, r, u);
+    if (sp.n_slots == 1) eval_cfg_hj<1>(sp, s_hj, coef_c, coef_d, s, p, r, u);
+    else if (sp.n_slots == 2) eval_cfg_hj<2>(sp, s_hj, coef_c, coef_d, s, p, r, u);
+    else eval_cfg_hj<3>(sp, s_hj, coef_c, coef_d, s, p, r, u);
   } else {
     if (sp.n_slots == 1) eval_cfg<1>(sp, ka, kb, w, j, s, p, r, u);
     else if (sp.n_slots == 2) eval_cfg<2>(sp, ka, kb, w, j, s, p, r, u);
@@ -787,14 +794,22 @@ __device__ __forceinline__ void eval_any(const SpaceParams& sp, const float* __r
   }
 }
 
+// One block per set: every config evaluated once (a config per thread per
+// pass), the block's max key (objective desc, config asc) found by a warp
+// then block reduction, and the thread that evaluated the winner writes its
+// RPerf / Throughput / Fairness -- no second evaluation. HJ: operands from the
+// basis rows (staged in shared memory) and the coefficient tables.
 template <bool HJ>
-__global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka, const float* __restrict__ kb,
-                              const float* __restrict__ w, const int64_t* __restrict__ set_ids,
-                              const unsigned long long* __restrict__ key_src, float* out_all,
-                              const unsigned long long* __restrict__ err, unsigned long long* hdr,
-                              const float* __restrict__ hj, const float* __restrict__ coef_c,
-                              const float* __restrict__ coef_d) {
+__global__ void __launch_bounds__(256) k_sets_detail(const SpaceParams sp, const float* __restrict__ ka,
+                                                     const float* __restrict__ kb, const float* __restrict__ w,
+                                                     const int64_t* __restrict__ set_ids,
+                                                     const unsigned long long* __restrict__ key_src, float* out_all,
+                                                     const unsigned long long* __restrict__ err,
+                                                     unsigned long long* hdr, const float* __restrict__ hj,
+                                                     const float* __restrict__ coef_c,
+                                                     const float* __restrict__ coef_d) {
   __shared__ unsigned long long s_key[32];
+  __shared__ float s_hj[3 * 12];
   float* out = out_all + (int64_t)blockIdx.x * 8;
   int64_t set_id;
   if (set_ids) {
@@ -819,7 +834,12 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
   if (sp.n_slots == 1) unrank_set<1>(set_id, j);
   else if (sp.n_slots == 2) unrank_set<2>(set_id, j);
   else unrank_set<3>(set_id, j);
+  if (HJ) {
+    if (threadIdx.x < 12 * sp.n_slots) s_hj[threadIdx.x] = hj[j[threadIdx.x / 12] * 12 + threadIdx.x % 12];
+    __syncthreads();
+  }
   unsigned long long key = 0;
+  float br[3] = {0.0f, 0.0f, 0.0f}, bu = 0.0f;  // the thread's best config's values
   if (sp.search_mode == 1) {  // the hill climb's choice (R22), not the exhaustive argmax
     if (threadIdx.x == 0) {
       float o;
@@ -827,51 +847,68 @@ __global__ void k_sets_detail(const SpaceParams sp, const float* __restrict__ ka
       if (sp.n_slots == 1) c = hill_search<1>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
       else if (sp.n_slots == 2) c = hill_search<2>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
       else c = hill_search<3>(sp, ka, kb, w, j, sp.hc_state, sp.hc_cap, &o, &ev);
-      key = c >= 0 ? (((unsigned long long)ord_float_d(o) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
+      if (c >= 0) {
+        key = ((unsigned long long)ord_float_d(o) << 32) | (0xFFFFFFFFull - (unsigned)c);
+        eval_any<HJ>(sp, ka, kb, w, s_hj, coef_c, coef_d, j, c / sp.n_caps, c % sp.n_caps, br, &bu);
+      }
     }
-  } else
-  for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
-    int s = c / sp.n_caps, p = c % sp.n_caps;
-    float r[3], u;
-    eval_any<HJ>(sp, ka, kb, w, hj, coef_c, coef_d, j, s, p, r, &u);
-    bool feas = true;
-    for (int i = 0; i < sp.n_slots; i++) feas = feas && (r[i] > 0.0f);
-    unsigned long long kk = feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
-    key = kk > key ? kk : key;
+  } else {
+    for (int c = threadIdx.x; c < sp.n_cfg; c += blockDim.x) {
+      const int s = c / sp.n_caps, p = c % sp.n_caps;
+      float r[3], u;
+      eval_any<HJ>(sp, ka, kb, w, s_hj, coef_c, coef_d, j, s, p, r, &u);
+      bool feas = true;
+      for (int i = 0; i < sp.n_slots; i++) feas = feas && (r[i] > 0.0f);
+      const unsigned long long kk =
+          feas ? (((unsigned long long)ord_float_d(u) << 32) | (0xFFFFFFFFull - (unsigned)c)) : 0ull;
+      if (kk > key) {
+        key = kk;
+        bu = u;
+        br[0] = r[0];
+        br[1] = r[1];
+        br[2] = r[2];
+      }
+    }
   }
+  const unsigned long long mine = key;
   key = warp_max_u64(key);
   if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = key;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long m = 0;
-    for (int w = 0; w < (int)(blockDim.x + 31) / 32; w++) m = s_key[w] > m ? s_key[w] : m;
-    if (m == 0) {
+  if (threadIdx.x < 32) {
+    const int nw = (blockDim.x + 31) >> 5;
+    unsigned long long v = threadIdx.x < nw ? s_key[threadIdx.x] : 0ull;
+    v = warp_max_u64(v);
+    if (threadIdx.x == 0) s_key[0] = v;
+  }
+  __syncthreads();
+  const unsigned long long m = s_key[0];
+  if (m == 0ull) {
+    if (threadIdx.x == 0) {
       out[0] = __int_as_float(-1);
       out[1] = -INFINITY;
       out[2] = out[3] = 0.0f;
-      return;
     }
-    int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
-    int s = c / sp.n_caps, p = c % sp.n_caps;
-    float thr = 0.0f, fair = INFINITY, u, r[3];
-    eval_any<HJ>(sp, ka, kb, w, hj, coef_c, coef_d, j, s, p, r, &u);
-    for (int i = 0; i < sp.n_slots; i++) {
-      float rp = __fmaf_rn(r[i], kInvScale, sp.alpha);
-      out[4 + i] = rp;
-      thr = (i == 0) ? rp : __fadd_rn(thr, rp);
-      fair = fminf(fair, rp);
-    }
-    out[0] = __int_as_float(c);
-    out[1] = u;
-    out[2] = thr;
-    out[3] = fair;
+    return;
   }
+  if (mine != m) return;  // exactly one thread holds the winning (unique) key
+  const int c = (int)(0xFFFFFFFFull - (m & 0xFFFFFFFFull));
+  float thr = 0.0f, fair = INFINITY;
+  for (int i = 0; i < sp.n_slots; i++) {
+    const float rp = __fmaf_rn(br[i], kInvScale, sp.alpha);
+    out[4 + i] = rp;
+    thr = (i == 0) ? rp : __fadd_rn(thr, rp);
+    fair = fminf(fair, rp);
+  }
+  out[0] = __int_as_float(c);
+  out[1] = bu;
+  out[2] = thr;
+  out[3] = fair;
 }
 
 void launch_sets_detail(const SpaceParams& sp, const float* ka, const float* kb, const float* w, const int64_t* set_ids,
                         int64_t n, float* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_sets_detail<false><<<(unsigned)n, 128, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out, nullptr, nullptr, nullptr,
+  k_sets_detail<false><<<(unsigned)n, 256, 0, st>>>(sp, ka, kb, w, set_ids, nullptr, out, nullptr, nullptr, nullptr,
                                                    nullptr, nullptr);
 }
 
@@ -882,10 +919,10 @@ void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb,
   // [2..5] the detail row -- the kernel writes it directly, no copy. tb != NULL:
   // operands from hj and the coefficient tables (no ka / kb this step)
   if (tb)
-    k_sets_detail<true><<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
+    k_sets_detail<true><<<1, 256, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
                                            host_out, hj, tb->coef_c, tb->coef_d);
   else
-    k_sets_detail<false><<<1, 128, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
+    k_sets_detail<false><<<1, 256, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
                                             host_out, nullptr, nullptr, nullptr);
 }
 

@@ -62,6 +62,12 @@ struct PairGrid {
   int64_t seg_t0[3], seg_end[3];
   int seg_per[3], seg_b[3];
   unsigned one;       // runtime 1: keeps the integer adds on the FMA pipe (IMAD)
+  // stage-split launches (SPLIT): unit u = stage group u % n_sg of whole tile
+  // t0 + u / n_sg; group q covers stages [q n_stages / n_sg, (q + 1) n_stages / n_sg).
+  // Each unit folds its best masked key per pair into merge[u / n_sg][j1 local][j0 local]
+  // as (key bits << 32 | ~stage) by atomicMax; k_pairs_merge_finish resolves them.
+  int n_sg;
+  unsigned long long* merge;
 };
 
 __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_t* I, int64_t* J) {
@@ -76,8 +82,25 @@ __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_
 
 // Work unit u of a launch with NB row groups (of 16 j1 rows) per unit -> tile
 // (I, J) and its first row group b0. NB = 4: whole tiles.
-template <int NB>
-__device__ __forceinline__ void unit_coords(const PairGrid& g, int64_t u, int64_t* I, int64_t* J, int* b0) {
+// last stage + 1 of stage-split unit u (recomputed from u: no loop-carried register)
+__device__ __forceinline__ int split_stage_hi(const PairGrid& g, int n_stages, int64_t u) {
+  return ((int)u % g.n_sg + 1) * n_stages / g.n_sg;
+}
+
+template <int NB, bool SPLIT>
+__device__ __forceinline__ void unit_coords(const PairGrid& g, int n_stages, int64_t u, int64_t* I, int64_t* J,
+                                            int* b0, int* s_lo, int* s_hi) {
+  *s_lo = 0;
+  *s_hi = n_stages;
+  if (SPLIT) {  // < 2^31 units (at most one round of CTA slots)
+    const int t = (int)u / g.n_sg;
+    const int q = (int)u - t * g.n_sg;
+    tile_coords(g, g.t0 + t, I, J);
+    *b0 = 0;
+    *s_lo = q * n_stages / g.n_sg;
+    *s_hi = (q + 1) * n_stages / g.n_sg;
+    return;
+  }
   if (NB == kM) {
     tile_coords(g, g.t0 + u, I, J);
     *b0 = 0;
@@ -107,7 +130,7 @@ __device__ __forceinline__ void issue_stage(float* stage, uint64_t* bar, const S
 
 }  // namespace
 
-template <int MINB, int NB>
+template <int MINB, int NB, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
                         const float* __restrict__ fast,
@@ -147,11 +170,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (int e = threadIdx.x; e < kTile * kBgRow; e += kThreads) sbg[e] = -1;
   __syncthreads();
   int64_t I, J;
-  int b0;
-  unit_coords<NB>(g, t, &I, &J, &b0);
-  int s = 0, buf = 0;
+  int b0, s_lo, s_hi;  // stages [s_lo, s_hi) of the unit (the whole config axis unless SPLIT)
+  unit_coords<NB, SPLIT>(g, sp.n_stages, t, &I, &J, &b0, &s_lo, &s_hi);
+  int s = s_lo, buf = 0;
+  (void)s_hi;
   unsigned phase = 0u;  // bit b = parity of the next wait on bars[b]
-  if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, 0);
+  if (threadIdx.x == 0) issue_stage(smem, &bars[0], sp, fast, I, J, s_lo);
 
   float breg[kM][NB];
 #pragma unroll
@@ -162,11 +186,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
   while (true) {
     // prefetch the next (tile, state) into the other buffer
     int64_t nt = t, nI = I, nJ = J;
-    int ns = s + 1, nb0 = b0;
-    if (ns == sp.n_stages) {
-      ns = 0;
+    int ns = s + 1, nb0 = b0, ns_lo = 0, ns_hi = 0;
+    if (ns == (SPLIT ? split_stage_hi(g, sp.n_stages, t) : sp.n_stages)) {
       nt = t + gridDim.x;
-      if (nt < g.n_units) unit_coords<NB>(g, nt, &nI, &nJ, &nb0);
+      if (nt < g.n_units) unit_coords<NB, SPLIT>(g, sp.n_stages, nt, &nI, &nJ, &nb0, &ns_lo, &ns_hi);
+      ns = SPLIT ? ns_lo : 0;
     }
     const bool has_next = nt < g.n_units;
     if (has_next && threadIdx.x == 0)
@@ -223,7 +247,31 @@ __global__ void __launch_bounds__(kThreads, MINB)
           sbg[(ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a] = (int16_t)s;
         }
 
-    if (s == sp.n_stages - 1) {
+    if (SPLIT && s == split_stage_hi(g, sp.n_stages, t) - 1) {
+      // ---- unit end: fold this stage group's best key per pair into the merge
+      // buffer (max key, then lowest stage = the canonical first maximum); the
+      // entries are the thread's own (no barrier), infeasible-only pairs skip
+      // park the keys in shared memory (unrolled stores), merge them in a rolled loop
+#pragma unroll
+      for (int a = 0; a < kM; a++)
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+          sbest[(ty + 16 * b) * kBgRow + tx + 16 * a] = breg[a][b];
+          breg[a][b] = 0.0f;
+        }
+      unsigned long long* mg = g.merge + ((int)t / g.n_sg) * (kTile * kTile);
+#pragma unroll 1
+      for (int ab = 0; ab < kM * NB; ab++) {
+        const int a = ab & 3, b = ab >> 2;
+        const int e = (ty + 16 * b) * kBgRow + tx + 16 * a;
+        const float m = sbest[e];
+        if (m > 0.0f)
+          atomicMax(mg + (ty + 16 * b) * kTile + tx + 16 * a,
+                    ((unsigned long long)__float_as_uint(m) << 32) | (0xFFFFFFFFull - (unsigned long long)(unsigned)sbg[e]));
+        sbg[e] = -1;
+      }
+    }
+    if (!SPLIT && s == sp.n_stages - 1) {
       // ---- tile end: park each pair's best key, then resolve and write with a
       // rolled loop in which a warp owns 32 consecutive j0 of one column
       // (128-byte coalesced obj/cfg writes)
@@ -286,10 +334,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (bc >= 0) {
             const unsigned long long kk = pack_key(bo, sid);
             key = kk > key ? kk : key;
+#ifndef COSCHED_VAR_NOFLAG
             if (bo < thr) {  // not provably within tau/2 of the FP32 argmax: exact re-score
               const unsigned at = atomicAdd(rb.n, 1u);
               if (at < rb.cap) rb.list[at] = (unsigned)k;
             }
+#endif
           }
         }
       }
@@ -307,11 +357,74 @@ __global__ void __launch_bounds__(kThreads, MINB)
   block_max_key(key, best_key);
 }
 
+// Resolution of the stage-split tiles (four blocks per tile): per pair the merged
+// (best masked key, first stage) gives the config -- stage and the key's low
+// bits, as in the tile end -- and the exact FP32 objective w0 + w1 of it; the
+// merge entries are reset for the next step. Writes obj / cfg, the rescore flag
+// and the block's best key.
+__global__ void __launch_bounds__(256) k_pairs_merge_finish(const SpaceParams sp, const PairGrid g,
+                                                             const float* __restrict__ w, float* __restrict__ out_obj,
+                                                             int32_t* __restrict__ out_cfg,
+                                                             unsigned long long* __restrict__ best_key,
+                                                             const unsigned long long* __restrict__ err,
+                                                             const RescoreBuf rb) {
+  if (*err != ~0ull) return;
+  int64_t I, J;
+  tile_coords(g, g.t0 + blockIdx.x, &I, &J);
+  unsigned long long* mg = g.merge + (int64_t)blockIdx.x * (kTile * kTile);
+  const float thr = rescore_threshold<2>(rb.wmm);
+  const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
+  constexpr int kPer = 4;  // pairs per thread, all loads in flight; blockIdx.y: which quarter of the tile
+  int c_[kPer];
+  float f0[kPer], f1[kPer];
+  const int e0 = blockIdx.y * (kTile * kTile / 4);
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    const int e = e0 + u * 256 + threadIdx.x, rj = e >> 6, ri = e & 63;
+    const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+    const unsigned long long v = mg[e];
+    mg[e] = 0ull;  // reset for the next step
+    const bool ok = j0 < j1 && j1 >= g.c0 && j1 < g.c1;
+    c_[u] = ok ? -1 : -2;
+    f0[u] = f1[u] = 0.0f;
+    if (ok && v) {
+      const int sg = (int)(0xFFFFFFFFull - (v & 0xFFFFFFFFull));
+      const int c = sg * kStageCfg + 31 - (int)((v >> 32) & 31u);
+      c_[u] = c;
+      const int st = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st * sp.n_caps;
+      f0[u] = __ldg(w + (int64_t)(st * npad + (int)j0) * rsz + p);
+      f1[u] = __ldg(w + (int64_t)(w1base + st * npad + (int)j1) * rsz + p);
+    }
+  }
+  unsigned long long key = 0ull;
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    if (c_[u] == -2) continue;
+    const int e = e0 + u * 256 + threadIdx.x, rj = e >> 6, ri = e & 63;
+    const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
+    const int c = c_[u];
+    const float bo = c >= 0 ? __fadd_rn(f0[u], f1[u]) : -INFINITY;
+    const int64_t sid = ((j1 * (j1 - 1)) >> 1) + j0, k = sid - g.first_set;
+    if (out_obj) out_obj[k] = bo;
+    if (out_cfg) out_cfg[k] = c;
+    if (c >= 0) {
+      const unsigned long long kk = pack_key(bo, sid);
+      key = kk > key ? kk : key;
+      if (bo < thr) {
+        const unsigned at = atomicAdd(rb.n, 1u);
+        if (at < rb.cap) rb.list[at] = (unsigned)k;
+      }
+    }
+  }
+  block_max_key(key, best_key);
+}
+
 // Precondition: tiled_applicable(2, n_jobs, first, count) (kernels.cu), i.e. the
 // shard is whole colex columns and the queue has < 32768 column tiles.
 int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* w, const float* fast, int64_t first,
                             int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,
-                            const unsigned long long* err, const RescoreBuf& rb, cudaStream_t st) {
+                            const unsigned long long* err, const RescoreBuf& rb, const PairMerge& merge,
+                            cudaStream_t st) {
   // column range of the shard; shards are whole columns (cosched_shard_range)
   auto c2 = [](int64_t n) { return n * (n - 1) / 2; };
   auto col_at = [&](int64_t v) {  // smallest c with C(c,2) >= v
@@ -332,18 +445,18 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   g.n_tiles = (jt1 + 1) * (jt1 + 2) / 2 - g.base;
   constexpr size_t smem = (size_t)2 * 6 * kTile * kStageRS * sizeof(float) +
                           (size_t)kTile * kBgRow * (sizeof(float) + sizeof(int16_t));
-  const char* fs = getenv("COSCHED_PAIR_SPLIT");  // testing knob: force the tail split (1, 2 or 4)
+  const char* fs = getenv("COSCHED_PAIR_SPLIT");  // testing knob: stage groups of the tail split (1 = none)
   const int forced_split = fs ? atoi(fs) : 0;
   const char* mb = getenv("COSCHED_PAIR_MINB");
   const int minb = (mb && mb[0] == '1') ? 1 : 2;
-  smem_optin((const void*)k_score_pairs_tiled<1, 4>, smem);
-  smem_optin((const void*)k_score_pairs_tiled<2, 4>, smem);
-  smem_optin((const void*)k_score_pairs_tiled<2, 2>, smem);
-  smem_optin((const void*)k_score_pairs_tiled<2, 1>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<1, 4, false>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 4, false>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 4, true>, smem);
+  smem_optin((const void*)k_score_pairs_tiled<2, 1, false>, smem);
   const int g_num_sms = num_sms();
   int per_sm = 0;
-  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1, 4>, kThreads, smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2, 4>, kThreads, smem);
+  if (minb == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<1, 4, false>, kThreads, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_pairs_tiled<2, 4, false>, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t slots = (int64_t)g_num_sms * per_sm;
   // Partial column blocks: the shard's first and last column blocks hold only
@@ -358,7 +471,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   Seg segs[3];
   int n_seg = 0;
   int64_t fa = 0, fb = g.n_tiles;  // whole tiles [fa, fb)
-  if (minb == 2 && forced_split == 0) {
+  if (minb == 2) {
     if (jt0 == jt1) {
       if (hi1 - lo0 < kM) {
         segs[n_seg++] = {0, g.n_tiles, hi1 - lo0, lo0};
@@ -376,33 +489,44 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     }
   }
   // Tail: whole-tile rounds leave slots - R CTAs idle for a
-  // whole tile time in the last round (R = whole tiles mod slots), which is
-  // what limits strong scaling once a rank has few tiles. The last R whole
-  // tiles can go to the unit launch as `split` units per tile (4/split row
-  // groups of 16 j1 rows each, disjoint outputs, no merge), split in {1, 2, 4}
-  // minimising ceil(split * R / slots) / split; with partial columns the unit
-  // launch has single-group units, so the split is 1 or 4.
+  // whole tile time in the last round (R = whole tiles mod slots), which is what
+  // limits strong scaling once a rank has few tiles. The last R tiles are split
+  // along the config axis instead: n_sg = min(n_stages, slots / R) units per
+  // tile, each scoring a contiguous group of stages of the whole tile and
+  // folding its per-pair best into the merge buffer; k_pairs_merge_finish then
+  // resolves those tiles. A stage group costs its share of the tile's per-stage
+  // work (TMA, barriers, bodies), unlike a row-group split, which pays every
+  // stage of the tile. COSCHED_PAIR_SPLIT = n forces n stage groups (1 = none).
   const int64_t n_full = fb - fa;
   const int64_t R = n_full > slots ? n_full % slots : n_full;
-  int split = 1;
-  if (R) {
-    double best = 1.0;
-    for (int h = 2; h <= kM; h *= 2) {
-      if (n_seg && h != kM) continue;
-      const double tt = (double)((h * R + slots - 1) / slots) / h;
-      if (tt < best - 1e-9) {
-        best = tt;
-        split = h;
+  // groups per tile: minimise the tail's length in stage times,
+  // ceil(R q / slots) rounds of units of ceil(n_stages / q) stages plus a unit's
+  // fixed cost (the merge atomics and the pipeline start, ~0.3 of a stage,
+  // measured on C4); q = 1 keeps whole tiles. Ties keep fewer, larger units.
+  int n_sg = 1;
+  if (R > 0 && merge.buf && minb == 2 && R <= merge.tiles) {
+    auto tail_len = [&](int q) {
+      return (double)((R * q + slots - 1) / slots) * ((sp.n_stages + q - 1) / q + (q > 1 ? 0.3 : 0.0));
+    };
+    double best = tail_len(1);
+    for (int q = 2; q <= sp.n_stages; q++)
+      if (tail_len(q) < best - 1e-9) {
+        best = tail_len(q);
+        n_sg = q;
       }
-    }
+    if (forced_split > 0) n_sg = std::min(forced_split, sp.n_stages);
   }
-  if (forced_split == 1 || forced_split == 2 || forced_split == 4) split = forced_split;
-  if (minb == 1) split = 1;
-  const int64_t n_whole = split == 1 ? n_full : n_full - R;
-  const int n_part = n_seg;
-  if (split > 1) segs[n_seg++] = {fa + n_whole, R, kM, 0};
-  const int unit_nb = (n_part == 0 && split == 2) ? 2 : 1;  // row groups per unit of the unit launch
+  const int64_t n_whole = n_sg > 1 ? n_full - R : n_full;
   int launches = 0;
+  // partial-column units on the side stream: their CTAs take the slots the
+  // whole-tile launch frees in its last round, next to the stage-split units
+  const bool fork = n_seg > 0 && merge.side && merge.ev_fork && merge.ev_join;
+  cudaStream_t ust = st;
+  if (fork) {
+    cudaEventRecord(merge.ev_fork, st);
+    cudaStreamWaitEvent(merge.side, merge.ev_fork, 0);
+    ust = merge.side;
+  }
   if (n_whole > 0) {
     launches++;
     g.t0 = fa;
@@ -410,15 +534,27 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     g.n_seg = 0;
     const int64_t grid = n_whole < slots ? n_whole : slots;
     if (minb == 1)
-      k_score_pairs_tiled<1, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+      k_score_pairs_tiled<1, 4, false><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
     else
-      k_score_pairs_tiled<2, 4><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+      k_score_pairs_tiled<2, 4, false><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+  }
+  if (n_sg > 1) {
+    launches += 3;
+    cudaMemsetAsync(merge.buf, 0, (size_t)R * kTile * kTile * sizeof(unsigned long long), st);
+    g.t0 = fa + n_whole;
+    g.n_units = R * n_sg;
+    g.n_sg = n_sg;
+    g.merge = merge.buf;
+    g.n_seg = 0;
+    const int64_t grid = g.n_units < slots ? g.n_units : slots;
+    k_score_pairs_tiled<2, 4, true><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+    k_pairs_merge_finish<<<dim3((unsigned)R, 4), 256, 0, st>>>(sp, g, w, obj, cfg, best_key, err, rb);
   }
   if (n_seg > 0) {
     launches++;
     int64_t end = 0;
     for (int q = 0; q < n_seg; q++) {
-      const int per = segs[q].groups / unit_nb;  // units per tile
+      const int per = segs[q].groups;  // single-row-group units
       end += segs[q].n * per;
       g.seg_t0[q] = segs[q].t0;
       g.seg_end[q] = end;
@@ -429,10 +565,11 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     g.t0 = 0;
     g.n_units = end;
     const int64_t grid = end < slots ? end : slots;
-    if (unit_nb == 2)
-      k_score_pairs_tiled<2, 2><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
-    else
-      k_score_pairs_tiled<2, 1><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+    k_score_pairs_tiled<2, 1, false><<<(unsigned)grid, kThreads, smem, ust>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+  }
+  if (fork) {
+    cudaEventRecord(merge.ev_join, merge.side);
+    cudaStreamWaitEvent(st, merge.ev_join, 0);
   }
   return launches;
 }

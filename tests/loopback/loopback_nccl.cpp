@@ -18,6 +18,7 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <map>
 #include <mutex>
@@ -32,6 +33,7 @@ struct Group {
   std::condition_variable cv;
   int arrived = 0;
   unsigned gen = 0;
+  bool broken = false;
   std::vector<std::vector<char>> slot;
 };
 
@@ -39,16 +41,25 @@ std::mutex g_mu;
 std::map<std::string, Group*> g_groups;
 std::atomic<unsigned long long> g_ids{0};
 
-void barrier(Group* g) {
+// false when a rank did not arrive within 60 s (it failed before the
+// collective): the group is marked broken and every later collective fails
+// fast, so the test reports the first error instead of hanging
+bool barrier(Group* g) {
   std::unique_lock<std::mutex> lk(g->m);
+  if (g->broken) return false;
   const unsigned gen = g->gen;
   if (++g->arrived == g->n) {
     g->arrived = 0;
     g->gen++;
     g->cv.notify_all();
-  } else {
-    g->cv.wait(lk, [&] { return g->gen != gen; });
+    return true;
   }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(60), [&] { return g->gen != gen || g->broken; }) || g->broken) {
+    g->broken = true;
+    g->cv.notify_all();
+    return false;
+  }
+  return true;
 }
 
 size_t type_size(int t) {
@@ -110,7 +121,7 @@ int ncclCommInitRank(ncclComm** comm, int nranks, ncclUniqueId id, int rank) {
     g = e;
   }
   if (g->n != nranks) return 4;
-  barrier(g);  // collective, like NCCL's init
+  if (!barrier(g)) return 1;  // collective, like NCCL's init
   *comm = new ncclComm{g, rank};
   return 0;
 }
@@ -129,7 +140,7 @@ int ncclAllReduce(const void* send, void* recv, size_t count, int dtype, int op,
   Group* g = c->g;
   g->slot[c->rank].resize(bytes);
   if (bytes && cuMemcpyDtoH(g->slot[c->rank].data(), (CUdeviceptr)send, bytes) != CUDA_SUCCESS) return 1;
-  barrier(g);
+  if (!barrier(g)) return 1;
   std::vector<char> acc(g->slot[0]);
   for (int r = 1; r < g->n; r++) {
     const void* x = g->slot[r].data();
@@ -143,7 +154,7 @@ int ncclAllReduce(const void* send, void* recv, size_t count, int dtype, int op,
       default: return 4;
     }
   }
-  barrier(g);  // every rank has read every slot before any slot is rewritten
+  if (!barrier(g)) return 1;  // every rank has read every slot before any slot is rewritten
   if (bytes && cuMemcpyHtoD((CUdeviceptr)recv, acc.data(), bytes) != CUDA_SUCCESS) return 1;
   return 0;
 }
@@ -155,11 +166,11 @@ int ncclAllGather(const void* send, void* recv, size_t count, int dtype, ncclCom
   Group* g = c->g;
   g->slot[c->rank].resize(bytes);
   if (bytes && cuMemcpyDtoH(g->slot[c->rank].data(), (CUdeviceptr)send, bytes) != CUDA_SUCCESS) return 1;
-  barrier(g);
+  if (!barrier(g)) return 1;
   std::vector<char> all((size_t)g->n * bytes);
   for (int r = 0; r < g->n; r++)
     if (bytes) memcpy(all.data() + (size_t)r * bytes, g->slot[r].data(), bytes);
-  barrier(g);
+  if (!barrier(g)) return 1;
   if (!all.empty() && cuMemcpyHtoD((CUdeviceptr)recv, all.data(), all.size()) != CUDA_SUCCESS) return 1;
   return 0;
 }

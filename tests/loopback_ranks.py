@@ -47,6 +47,7 @@ def one_rank(pb, Fd, uid, r, W, k, truth, out, errs):
 
 
 def run_case(pb, F, W, k, truth):
+    print(f"case {pb.name} n={F.shape[0]} W={W} k={k}", file=sys.stderr, flush=True)
     Fd = torch.from_numpy(np.ascontiguousarray(F)).cuda()
     torch.cuda.synchronize()
     ref = {}
@@ -76,6 +77,8 @@ def run_case(pb, F, W, k, truth):
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(400, exit=True)  # a hang prints every thread's stack
     W = int(sys.argv[1])
     report = []
     pb, F = bench_config("C3")

@@ -80,7 +80,16 @@ def test_shards_partition_whole_columns(cs, n, k):
                 assert cols
         assert nxt == total
         if total >= 1000 * W and k == 2:
-            assert max(sizes) - min(sizes) <= 2 * max(math.comb(n - 1, k - 1), 1)  # one column each side
+            # pairs: whole 64-column blocks (cosched.h), chosen to balance the scorer's
+            # modelled time -- per-rank tile counts within two column blocks' tiles
+            bounds = [next(c for c in range(n + 1) if math.comb(c, 2) >= a) for a in
+                      [sum(sizes[:r]) for r in range(W)]] + [n]
+            assert all(b % 64 == 0 for b in bounds[1:-1])
+            nb = -(-n // 64)
+            blk = [-(-b // 64) for b in bounds]
+            tiles = [blk[r + 1] * (blk[r + 1] + 1) // 2 - blk[r] * (blk[r] + 1) // 2 for r in range(W)]
+            assert sum(tiles) == nb * (nb + 1) // 2
+            assert max(tiles) - min(tiles) <= 2 * nb
         if total >= 1000 * W and k == 3:
             # triples balance the scorer's 64 x 64 tiles per plane (cosched.h): per-rank
             # tile counts within one plane's tiles of each other

@@ -23,7 +23,7 @@ def test_w_ranks_through_loopback_equal_single_rank(W):
     import loopback
     env = dict(os.environ, COSCHED_NCCL_LIB=loopback.build())
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "loopback_ranks.py"), str(W)], env=env,
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     rep = json.loads(r.stdout.strip().splitlines()[-1])
     assert [c["W"] for c in rep] == [W] * 5

@@ -391,12 +391,13 @@ def test_fast_scorer_equals_generic(cs, n_slots, n):
     assert s0.local_best_key() == s1.local_best_key()
 
 
-@pytest.mark.parametrize("split", ["1", "2", "4"])
+@pytest.mark.parametrize("split", ["1", "2", "4", "15"])
 @pytest.mark.parametrize("W", [1, 3])
 def test_pair_tail_split_units(cs, split, W, monkeypatch):
-    """The pair scorer's tail tiles as 1, 2 or 4 row-group units per tile (a second
-    launch, disjoint outputs) give the generic kernel's results on every set of every
-    fake rank (n = 1501: 24 column tiles, 300 tiles, a ragged last column)."""
+    """The pair scorer's last-round tiles split into 1, 2, 4 or 15 stage groups per
+    tile (units merged per pair by atomicMax, then resolved by k_pairs_merge_finish)
+    give the generic kernel's results on every set of every fake rank (n = 1501: 24
+    column tiles, 300 tiles, a ragged last column; 15 stages of 20 configs)."""
     monkeypatch.setenv("COSCHED_PAIR_SPLIT", split)
     pb = make_problem("b200", "c21", coef_seed=71, alpha=0.5)
     F, _ = make_features(1501, seed=71)
