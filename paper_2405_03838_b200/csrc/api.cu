@@ -6,6 +6,7 @@
 // reads back the few bytes of each result.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -76,6 +77,13 @@ bool nccl_load(std::string* why) {
 }
 
 thread_local std::string g_create_error;
+
+// NVTX range around each C-ABI entry point (header-only NVTX v3: a no-op
+// unless a profiler injects itself), so Nsight timelines show the API calls
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
   int prev = -1;
@@ -271,7 +279,7 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.wmm = (unsigned*)take(2 * kMaxSlots * sizeof(unsigned));
   w.best_key = (unsigned long long*)take(8);
   w.err = (unsigned long long*)take(8);
-  w.counters = (int64_t*)take(8 * 8);
+  w.counters = (int64_t*)take(16 * 8);  // [8]: keys through the greedy scan (instrumentation)
   w.job_key = (unsigned long long*)take((size_t)n_jobs * 8);
   w.taken = (uint32_t*)take((size_t)n_jobs * 4);
   w.picked = (unsigned long long*)take((size_t)n_jobs * 8 + 8);
@@ -696,6 +704,7 @@ static cosched_status allreduce_max(cosched_t h, void* dev, size_t count, int dt
 cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t n_rows, const int32_t* jobs_dev,
                                  int64_t n_jobs, void* workspace_dev, size_t workspace_bytes, const cosched_out* out,
                                  void* cuda_stream) {
+  NvtxRange nvtx_("cosched_score_all");
   if (!h) return COSCHED_E_ARG;
   h->err.clear();
   if (n_jobs < 0 || n_rows < 0 || (n_jobs > 0 && !features_dev) || (!jobs_dev && n_rows < n_jobs))
@@ -863,6 +872,7 @@ static cosched_status detail_rows(cosched_t h, const int64_t* ids, int64_t n, st
 }
 
 cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj) {
+  NvtxRange nvtx_("cosched_best_set");
   if (!h) return COSCHED_E_ARG;
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
   DeviceGuard g(h->device);
@@ -896,6 +906,7 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
 
 cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, float* obj, float* rperf,
                                    float* throughput, float* fairness) {
+  NvtxRange nvtx_("cosched_best_config");
   if (!h) return COSCHED_E_ARG;
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
   if (set_id < 0 || set_id >= cosched::n_sets(h->n_jobs, h->n_slots)) return fail(h, COSCHED_E_ARG, "set id out of range");
@@ -962,7 +973,9 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   // sets whose jobs are all still free are compacted and sorted
   // batch sizes grow geometrically from 8 M keys (a first batch that already holds
   // the k picks sorts little; deep scans reach 64 M keys per batch after 3 rounds)
-  int64_t batch_keys = (int64_t)64 << 20, batch_first = (int64_t)8 << 20;
+  // first batch 1 M keys, doubling (tools/greedy_stats.py on C4: 17.4 M keys sorted
+  // in 6 batches against 26.8 M in 3 with an 8 M first batch)
+  int64_t batch_keys = (int64_t)64 << 20, batch_first = (int64_t)1 << 20;
   if (const char* e = getenv("COSCHED_GREEDY_BATCH")) batch_keys = batch_first = std::max<int64_t>(1024, atoll(e));
   const int64_t kBatchMax = std::min<int64_t>(ws.batch_cap, batch_keys);
   int64_t kBatch = std::min<int64_t>(kBatchMax, batch_first);
@@ -971,6 +984,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   int64_t* np_dev = ws.counters + 1;
   unsigned long long* nk_dev = (unsigned long long*)(ws.counters + 2);
   CK(cudaMemsetAsync(np_dev, 0, 8, s));
+  CK(cudaMemsetAsync(ws.counters + 8, 0, 8, s));
   int bin_hi = kHistBins - 1;
   int64_t n_picks = 0;
   bool endgame = false;
@@ -996,15 +1010,23 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     const int64_t n_free = N - (int64_t)ns * n_picks;
     const int64_t n_comb = cosched::n_sets(n_free, ns);
     endgame = n_picks > 0 && n_comb <= kBatchMax && n_comb * 8 <= cosched::n_sets(N, ns);  // gathers << a full scan
-    // 3. compact this rank's keys in the range (or of the free jobs); gather over ranks; sort; scan
+    // 3. compact this rank's keys in the range (or of the free jobs); gather over ranks; sort; scan.
+    // The list keys are relative to the batch's lowest objective (fewer radix bits)
+    // and carry the jobs packed for pairs (GKeyFmt)
     CK(cudaMemsetAsync(nk_dev, 0, 8, s));
+    GKeyFmt fmt;
     if (endgame) {
+      fmt = gkey_format(ns, N, 0u, 1ull << 32);
       launch_free_sets(ns, taken_bits, N, (int32_t*)ws.job_key, ws.counters + 5, n_comb, h->out_obj, h->first,
-                       h->n_sets, (unsigned long long*)ws.alive, nk_dev, s);
+                       h->n_sets, (unsigned long long*)ws.alive, nk_dev, fmt, s);
       h->launches += 2;
     } else {
+      unsigned u_lo;
+      unsigned long long width;
+      bin_range_ord(mmh[0], mmh[1], bin_lo, bin_hi, &u_lo, &width);
+      fmt = gkey_format(ns, N, u_lo, width);
       launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
-                           (unsigned long long*)ws.alive, nk_dev, s);
+                           (unsigned long long*)ws.alive, nk_dev, fmt, s);
       h->launches++;
     }
     int64_t nk = 0;
@@ -1031,32 +1053,51 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       sorted = ws.gath_sorted;
       m = mx * W;
     }
-    CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s));
+    CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s, fmt.end_bit));
     h->launches++;
-    // scan the sorted list in chunks; between chunks drop (order-preserving)
-    // every key whose set touches a job taken meanwhile
-    unsigned long long* cur = sorted;
-    unsigned long long* spare = h->comm ? ws.gath : (unsigned long long*)ws.alive;
-    const int64_t kChunk = getenv("COSCHED_GREEDY_CHUNK") ? atoll(getenv("COSCHED_GREEDY_CHUNK")) : (1 << 16);
-    while (m > 0 && n_picks < k) {
-      const int64_t len = std::min<int64_t>(m, kChunk);
-      CK(launch_greedy_scan(ns, cur, len, N, taken_bits, ws.picked, np_dev, k, s));
+    // scan the sorted list in windows of kWin keys: the first window as it is
+    // (its keys were free at the batch start), every later window after an
+    // order-preserving select of the keys still free (a full-GPU pass over that
+    // window only), its count read by the scan from the device -- rounds are
+    // enqueued without host round trips; the scan returns at once after k picks.
+    // Every key is selected at most once, and only keys free at their window's
+    // start reach the one-block scan.
+    unsigned long long* S = h->comm ? ws.gath : (unsigned long long*)ws.alive;
+    int64_t* cnt_dev = ws.counters + 3;
+    const int64_t kWin = getenv("COSCHED_GREEDY_CHUNK") ? std::max<int64_t>(1024, atoll(getenv("COSCHED_GREEDY_CHUNK")))
+                                                       : (int64_t)1 << 18;
+    // windows grow from kWin0 (the batch's first keys are all free at its start:
+    // the first windows are where the batch's picks happen and block the most)
+    const int64_t kWin0 = getenv("COSCHED_GREEDY_WIN0") ? std::max<int64_t>(1024, atoll(getenv("COSCHED_GREEDY_WIN0")))
+                                                       : (int64_t)1 << 14;
+    int r = 0;
+    int64_t win = std::min(kWin0, kWin);
+    for (int64_t pos = 0; pos < m; pos += win, win = std::min(kWin, 2 * win), r++) {
+      const int64_t w = std::min<int64_t>(win, m - pos);
+      if (pos == 0) {
+        CK(launch_greedy_scan(ns, sorted, w, nullptr, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
+      } else {
+        CK(select_free_keys(ns, ws.sort_tmp, ws.sort_tmp_bytes, sorted + pos, S, cnt_dev, w, taken_bits, fmt, s));
+        CK(launch_greedy_scan(ns, S, w, cnt_dev, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
+        h->launches++;
+      }
       h->launches++;
       h->greedy_rounds++;
-      CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
-      if (m > len) {
-        CK(select_free_keys(ns, ws.sort_tmp, ws.sort_tmp_bytes, cur + len, spare, ws.counters + 3, m - len, taken_bits,
-                            s));
-        h->launches++;
-        CK(cudaMemcpyAsync(&m, ws.counters + 3, 8, cudaMemcpyDeviceToHost, s));
-        std::swap(cur, spare);
-      } else {
-        m = 0;
+      if ((r & 7) == 7 || pos + win >= m) {  // a host look at the pick count every 8 windows
+        CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (n_picks >= k) break;
       }
-      CK(cudaStreamSynchronize(s));
     }
     bin_hi = bin_lo - 1;
     kBatch = std::min<int64_t>(kBatchMax, kBatch * 2);
+  }
+  if (getenv("COSCHED_GREEDY_STATS")) {
+    int64_t scanned = 0;
+    CK(cudaMemcpyAsync(&scanned, ws.counters + 8, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "greedy: %lld picks, %lld keys through the scan, %lld windows\n", (long long)n_picks,
+            (long long)scanned, (long long)h->greedy_rounds);
   }
   picks->resize(n_picks);
   if (n_picks) {
@@ -1068,6 +1109,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
 
 cosched_status cosched_best_allocation(cosched_t h, int32_t k, int64_t* set_ids, int32_t* cfgs, double* total_obj,
                                        int32_t* n_found) {
+  NvtxRange nvtx_("cosched_best_allocation");
   if (!h || k < 1 || !set_ids) return fail(h, COSCHED_E_ARG, "bad allocation arguments");
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
   DeviceGuard g(h->device);
@@ -1317,6 +1359,7 @@ cosched_status cosched_node_workspace_size(cosched_t h, int64_t n_gpus, int32_t 
 cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* set_ids, int32_t gpus_per_node,
                                    double node_power_w, int32_t objective, void* workspace, size_t workspace_bytes,
                                    int32_t* caps_out, int32_t* cfgs_out, float* node_obj, void* cuda_stream) {
+  NvtxRange nvtx_("cosched_node_budget");
   if (!h) return COSCHED_E_ARG;
   if (n_gpus < 1 || !set_ids || !caps_out || !cfgs_out || !node_obj || gpus_per_node < 1 ||
       n_gpus % gpus_per_node != 0 || (objective != 1 && objective != 2))
@@ -1358,6 +1401,7 @@ cosched_status cosched_evaluate_truth(cosched_t h, const cosched_truth_desc* tru
                                       int64_t n_rows, const int32_t* jobs_dev, void* workspace,
                                       size_t workspace_bytes, const cosched_eval_out* out,
                                       cosched_eval_summary* summary, void* cuda_stream) {
+  NvtxRange nvtx_("cosched_evaluate_truth");
   if (!h) return COSCHED_E_ARG;
   if (!truth || !features_dev || !out || !out->prop_obj || !out->prop_fair || !out->best_obj || !out->worst_obj)
     return fail(h, COSCHED_E_ARG, "null argument");
@@ -1409,6 +1453,7 @@ cosched_status cosched_fit_workspace_size(const cosched_fit_desc* desc, size_t* 
 
 cosched_status cosched_fit(const cosched_fit_desc* desc, void* workspace, size_t workspace_bytes,
                            const cosched_fit_out* out, void* cuda_stream) {
+  NvtxRange nvtx_("cosched_fit");
   g_fit_error.clear();
   cosched_status st = fit_validate_desc(desc);
   if (st != COSCHED_OK) {

@@ -107,7 +107,7 @@ struct Workspace {
   int64_t* alive = nullptr;                // [n_sets_local] greedy alive list
   int64_t* alive2 = nullptr;               // [n_sets_local]
   unsigned long long* picked = nullptr;    // [n_jobs] greedy picked keys
-  int64_t* counters = nullptr;             // [8] device counters
+  int64_t* counters = nullptr;             // [16] device counters
   unsigned* hist = nullptr;                // [kHistBins] greedy objective histogram
   unsigned* mm = nullptr;                  // [2] min / max ord(obj)
   unsigned long long* gath = nullptr;      // [nranks * batch_cap] gathered keys (multi-rank)
@@ -130,23 +130,37 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
 // greedy.cu
 void launch_obj_minmax(const float* obj, int64_t count, unsigned* mm, cudaStream_t st);
 void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nbins, unsigned* hist, cudaStream_t st);
+// Greedy-list keys (greedy.cu): ((ord(obj) - base) << 32) | (0xFFFFFFFF - low), low =
+// (j1 << 16) | j0 for pairs of queues <= 65536 jobs (packed: the jobs decode with
+// two shifts; colex order of (j1, j0) equals set-id order) else the set id. Orders
+// exactly like the canonical packed key; a batch sorts only end_bit low bits.
+struct GKeyFmt {
+  int packed = 0;
+  unsigned base = 0;
+  int end_bit = 64;
+};
+GKeyFmt gkey_format(int n_slots, int64_t n_jobs, unsigned base, unsigned long long span_ord);
 void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
-                          unsigned long long* n_keys, cudaStream_t st);
+                          unsigned long long* n_keys, const GKeyFmt& fmt, cudaStream_t st);
+// [lo ord, hi ord) of histogram bins [bin_lo, bin_hi] given the objective range mm = (lo, hi)
+void bin_range_ord(unsigned lo, unsigned hi, int bin_lo, int bin_hi, unsigned* u_lo, unsigned long long* width);
 // greedy endgame: keys of every feasible set of free jobs (free list built on the device)
 void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
                       int64_t n_comb, const float* obj, int64_t first, int64_t count, unsigned long long* keys,
-                      unsigned long long* n_keys, cudaStream_t st);
+                      unsigned long long* n_keys, const GKeyFmt& fmt, cudaStream_t st);
 size_t sort_temp_bytes(int64_t n);
 size_t select_temp_bytes(int64_t n);
 cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const unsigned long long* in,
                              unsigned long long* out, int64_t* n_out, int64_t n, const uint32_t* taken_bits,
-                             cudaStream_t st);
+                             const GKeyFmt& fmt, cudaStream_t st);
 cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
-                           int64_t n, cudaStream_t st);
-cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
-                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
-                               cudaStream_t st);
+                           int64_t n, cudaStream_t st, int end_bit = 64);
+// picks are written as canonical packed keys (cosched_pack_key); the list length is
+// *m_dev when m_dev != NULL (a count produced on the device), else m
+cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, const int64_t* m_dev,
+                               int64_t n_jobs, uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks,
+                               int64_t k_max, const GKeyFmt& fmt, cudaStream_t st, int64_t* scanned = nullptr);
 int64_t pad_jobs(int64_t n_jobs);
 // node.cu
 size_t node_workspace_bytes(int64_t n_gpus, int32_t n_caps, int32_t U, int32_t gpus_per_node);

@@ -79,6 +79,55 @@ __device__ __forceinline__ int bin_of(unsigned u, unsigned lo, unsigned span, do
   return b;
 }
 
+// ---- greedy-list keys (cosched_internal.h GKeyFmt) ----
+GKeyFmt gkey_format(int n_slots, int64_t n_jobs, unsigned base, unsigned long long span_ord) {
+  GKeyFmt f;
+  f.packed = (n_slots == 2 && n_jobs <= 65536) ? 1 : 0;
+  f.base = base;
+  int bits = 0;
+  while (bits < 32 && (span_ord >> bits) > 1ull) bits++;  // ord - base < span_ord <= 2^bits
+  if (span_ord > (1ull << bits)) bits++;
+  f.end_bit = 32 + (bits > 32 ? 32 : bits);
+  return f;
+}
+
+void bin_range_ord(unsigned lo, unsigned hi, int bin_lo, int bin_hi, unsigned* u_lo, unsigned long long* width) {
+  const unsigned long long span = (unsigned long long)(hi - lo);
+  auto start = [&](int b) {
+    return (unsigned long long)lo + (((unsigned long long)b * (span + 1ull) + ((1ull << kHistLog2) - 1ull)) >> kHistLog2);
+  };
+  *u_lo = (unsigned)start(bin_lo);
+  *width = start(bin_hi + 1) - start(bin_lo);
+}
+
+template <int NS>
+__device__ __forceinline__ unsigned long long gkey_make(const GKeyFmt& f, float o, int64_t sid, const int64_t* j) {
+  const unsigned low = (NS == 2 && f.packed) ? (((unsigned)j[1] << 16) | (unsigned)j[0]) : (unsigned)sid;
+  return ((unsigned long long)(ord_float_d(o) - f.base) << 32) | (0xFFFFFFFFull - low);
+}
+template <int NS>
+__device__ __forceinline__ void gkey_jobs(const GKeyFmt& f, unsigned long long key, int32_t* jb) {
+  const unsigned low = 0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull);
+  if (NS == 2 && f.packed) {
+    jb[0] = (int32_t)(low & 0xFFFFu);
+    jb[1] = (int32_t)(low >> 16);
+    return;
+  }
+  int64_t j[3];
+  unrank_set<NS>((int64_t)low, j);
+#pragma unroll
+  for (int q = 0; q < NS; q++) jb[q] = (int32_t)j[q];
+}
+// the canonical packed key (pack_key) of a greedy-list key whose jobs are jb
+template <int NS>
+__device__ __forceinline__ unsigned long long gkey_canonical(const GKeyFmt& f, unsigned long long key,
+                                                             const int32_t* jb) {
+  const float o = unord_float_d((unsigned)(key >> 32) + f.base);
+  int64_t sid = (int64_t)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull));
+  if (NS == 2 && f.packed) sid = c2(jb[1]) + jb[0];
+  return pack_key(o, sid);
+}
+
 // Histogram privatised per block in shared memory (64 KB), merged with one
 // global atomic per nonzero bin and block.
 __global__ void __launch_bounds__(1024) k_obj_hist(const float* __restrict__ obj, int64_t count,
@@ -115,15 +164,19 @@ __global__ void __launch_bounds__(1024) k_obj_hist(const float* __restrict__ obj
 constexpr int kKirWarps = 8;
 constexpr int kKirQueue = 32 + 4 * 32;
 constexpr int kKirLoads = 4;
+constexpr int kKirOut = 256;
 template <int NS>
 __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* __restrict__ obj, int64_t first,
                                                                  int64_t count, const unsigned* __restrict__ mm,
                                                                  int nbins, int bin_lo, int bin_hi,
                                                                  const uint32_t* __restrict__ taken_bits,
                                                                  unsigned long long* keys,
-                                                                 unsigned long long* n_keys) {
+                                                                 unsigned long long* n_keys, const GKeyFmt fmt) {
   __shared__ int64_t s_id[kKirWarps][kKirQueue];
   __shared__ float s_o[kKirWarps][kKirQueue];
+  // per-warp output buffer: the free keys leave in runs of up to kKirOut with
+  // one atomicAdd per run (a single global counter takes every batch's keys)
+  __shared__ unsigned long long s_out[kKirWarps][kKirOut];
   const unsigned lo = mm[0], span = mm[1] - mm[0];
   const unsigned long long u_lo = bin_start(lo, span, bin_lo), u_hi = bin_start(lo, span, bin_hi + 1);  // [u_lo, u_hi)
   // one 32-bit unsigned compare: u_lo <= hi < 2^32 and u_hi - u_lo <= span + 1 < 2^32;
@@ -134,6 +187,17 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   float* qo = s_o[wib];
   int qn = 0;  // warp-uniform queue length
   auto in_range = [&](float o) { return ord_float_d(o) - r_lo < r_w; };
+  unsigned long long* ob = s_out[wib];
+  int on = 0;  // warp-uniform output buffer length
+  auto flush = [&]() {
+    if (on == 0) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(n_keys, (unsigned long long)on);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int e = lane; e < on; e += 32) keys[base + e] = ob[e];
+    __syncwarp();
+    on = 0;
+  };
   // decode the 32 queue entries [qn - n, qn) (n <= 32), append the free ones
   auto drain = [&](int n) {
     unsigned long long kk = 0ull;
@@ -145,17 +209,14 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
       ok = true;
 #pragma unroll
       for (int q = 0; q < NS; q++) ok = ok && !((__ldg(taken_bits + (j[q] >> 5)) >> (j[q] & 31)) & 1u);
-      if (ok) kk = pack_key(qo[qn - n + lane], sid);
+      if (ok) kk = gkey_make<NS>(fmt, qo[qn - n + lane], sid, j);
     }
     const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
-    if (m) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(n_keys, (unsigned long long)__popc(m));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      if (ok) keys[base + __popc(m & ((1u << lane) - 1u))] = kk;
-    }
+    if (ok) ob[on + __popc(m & ((1u << lane) - 1u))] = kk;
+    on += __popc(m);
     __syncwarp();
     qn -= n;
+    if (on > kKirOut - 32) flush();
   };
   auto push = [&](bool hit, float o, int64_t sid) {
     const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
@@ -199,6 +260,7 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
     while (qn >= 32) drain(32);
   }
   if (qn > 0) drain(qn);
+  flush();
 }
 
 // Endgame of the greedy: once few jobs are free, the sets that can still be
@@ -232,7 +294,8 @@ __global__ void k_free_list(const uint32_t* __restrict__ taken_bits, int64_t n_j
 
 template <int NS>
 __global__ void k_free_sets(const int32_t* __restrict__ free_list, int64_t n_comb, const float* __restrict__ obj,
-                            int64_t first, int64_t count, unsigned long long* keys, unsigned long long* n_keys) {
+                            int64_t first, int64_t count, unsigned long long* keys, unsigned long long* n_keys,
+                            const GKeyFmt fmt) {
   const int lane = threadIdx.x & 31;
   // a warp covers 32 consecutive ranks (whole-warp ballots); r0 is this warp's first
   for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; r0 < n_comb;
@@ -243,17 +306,17 @@ __global__ void k_free_sets(const int32_t* __restrict__ free_list, int64_t n_com
     if (r < n_comb) {
       int64_t q[3];
       unrank_set<NS>(r, q);  // ascending positions in the free list
-      int64_t sid = 0;
+      int64_t sid = 0, jv[3];
 #pragma unroll
       for (int i = 0; i < NS; i++) {
-        const int64_t jv = free_list[q[i]];
-        sid += (i == 0) ? jv : (i == 1 ? c2(jv) : c3(jv));  // colex rank of the ascending job tuple
+        jv[i] = free_list[q[i]];
+        sid += (i == 0) ? jv[i] : (i == 1 ? c2(jv[i]) : c3(jv[i]));  // colex rank of the ascending job tuple
       }
       if (sid >= first && sid < first + count) {
         const float o = obj[sid - first];
         if (o > -INFINITY) {
           ok = true;
-          kk = pack_key(o, sid);
+          kk = gkey_make<NS>(fmt, o, sid, jv);
         }
       }
     }
@@ -269,176 +332,188 @@ __global__ void k_free_sets(const int32_t* __restrict__ free_list, int64_t n_com
 
 void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
                       int64_t n_comb, const float* obj, int64_t first, int64_t count, unsigned long long* keys,
-                      unsigned long long* n_keys, cudaStream_t st) {
+                      unsigned long long* n_keys, const GKeyFmt& fmt, cudaStream_t st) {
   k_free_list<<<1, 1024, 0, st>>>(taken_bits, n_jobs, free_list, n_free_dev);
   if (n_comb <= 0) return;
   const unsigned blocks = (unsigned)std::min<int64_t>((n_comb + 255) / 256, 148 * 8);
   if (n_slots == 2)
-    k_free_sets<2><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys);
+    k_free_sets<2><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys, fmt);
   else
-    k_free_sets<3><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys);
+    k_free_sets<3><<<blocks, 256, 0, st>>>(free_list, n_comb, obj, first, count, keys, n_keys, fmt);
 }
 
-// The sequential rule over a sorted window of 1024 candidates, resolved in
-// parallel: an undecided candidate whose jobs are all still free and that is
-// the lowest-index undecided candidate on every one of its jobs cannot be
-// blocked by any earlier candidate, so it is taken; candidates touching a job
-// just taken are dropped; repeat until the window is decided. The taken set is
-// exactly the sequential greedy's, and picks are emitted in window (key) order.
+// The sequential rule over the sorted keys, window by window (kScanWin keys):
+//  1. filter, all threads: every key of the window is decoded (colex
+//     unranking) and tested against the taken bitmask (shared memory); keys
+//     with a taken job can never be picked (the greedy only takes sets whose
+//     jobs are all free) and are dropped;
+//  2. the survivors are compacted in key order (block ballots + prefix sum);
+//  3. warp 0 walks the survivors in order, 32 at a time: the first survivor
+//     of the group whose jobs are all free is taken (it is the sequential
+//     rule's next pick: every earlier key was blocked), its jobs are marked,
+//     the group's survivors sharing one of them are dropped, repeat. Picks are
+//     appended in key order; the scan stops at k_max.
+// Only keys still free at their window's start reach the sequential part --
+// 21,033 of the 5x10^7 keys of C4 (tools/greedy_stats.py) -- so the scan costs
+// about one decode per key. The taken bitmask (n_jobs bits) is the only
+// per-job state: any queue the set scorer accepts fits shared memory.
+constexpr int kScanThreads = 512, kScanPer = 4, kScanWin = kScanThreads * kScanPer, kScanWarps = kScanThreads / 32;
+
 template <int NS>
-__global__ void __launch_bounds__(1024, 1)
-    k_greedy_scan(const unsigned long long* __restrict__ sorted, int64_t m, int64_t n_jobs, uint32_t* taken_g,
-                  unsigned long long* picks, int64_t* n_picks, int64_t k_max) {
-  constexpr int CPT = 4;            // candidates per thread: window = 4096 keys
-  constexpr int WIN = 1024 * CPT;
-  extern __shared__ uint32_t s_dyn[];
-  uint32_t* s_taken = s_dyn;                                                    // n_jobs bits
-  uint32_t* s_first = s_dyn + ((n_jobs + 31) >> 5);  // n_jobs: round-stamped claims
-  __shared__ int32_t s_wsum[32];
-  __shared__ int64_t s_np;
-  const int words = (int)((n_jobs + 31) >> 5);
-  for (int i = threadIdx.x; i < words; i += blockDim.x) s_taken[i] = taken_g[i];
-  for (int i = threadIdx.x; i < n_jobs; i += blockDim.x) s_first[i] = 0u;
-  unsigned rnd = 1;  // round stamp (< 2^20 rounds per launch)
-  if (threadIdx.x == 0) s_np = *n_picks;
-  __syncthreads();
-  const int t = threadIdx.x;
-  unsigned long long nxt[CPT];
+__device__ __forceinline__ bool key_jobs_free(const GKeyFmt& f, unsigned long long key, const uint32_t* bits,
+                                              int32_t* jb) {
+  gkey_jobs<NS>(f, key, jb);
+  bool fr = true;
 #pragma unroll
-  for (int u = 0; u < CPT; u++) {
-    const int64_t i = (int64_t)t * CPT + u;
+  for (int q = 0; q < NS; q++) fr = fr && !((bits[jb[q] >> 5] >> (jb[q] & 31)) & 1u);
+  return fr;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kScanThreads, 1)
+    k_greedy_scan(const unsigned long long* __restrict__ sorted, int64_t m_host, const int64_t* __restrict__ m_dev,
+                  int64_t n_jobs, uint32_t* taken_g, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
+                  const GKeyFmt fmt, int64_t* scanned) {
+  int64_t np = *n_picks;  // warp 0's running count (uniform in warp 0)
+  if (np >= k_max) return;  // uniform: enqueued windows after the k-th pick cost one launch
+  const int64_t m = m_dev ? *m_dev : m_host;
+  if (scanned && threadIdx.x == 0) atomicAdd((unsigned long long*)scanned, (unsigned long long)m);
+  extern __shared__ __align__(16) unsigned long long s_dyn[];
+  unsigned long long* s_surv = s_dyn;                          // [kScanWin] survivors of a window
+  uint32_t* s_taken = reinterpret_cast<uint32_t*>(s_dyn + kScanWin);  // n_jobs bits
+  __shared__ int s_cnt[kScanPer * (kScanThreads / 32)];
+  constexpr int kCntPerLane = kScanPer * (kScanThreads / 32) / 32;  // the prefix pass: counts per lane of warp 0
+  __shared__ int s_n;
+  __shared__ int s_stop;
+  const int words = (int)((n_jobs + 31) >> 5);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int i = t; i < words; i += kScanThreads) s_taken[i] = taken_g[i];
+  if (t == 0) s_stop = 0;
+  unsigned long long nxt[kScanPer];
+#pragma unroll
+  for (int u = 0; u < kScanPer; u++) {
+    const int64_t i = (int64_t)u * kScanThreads + t;
     nxt[u] = i < m ? sorted[i] : 0ull;
   }
-  for (int64_t base = 0; base < m; base += WIN) {
-    if (s_np >= k_max) break;
-    unsigned long long key[CPT];
-    int32_t jb[CPT][3];
-    bool und[CPT], acc[CPT];
+  __syncthreads();
+  for (int64_t base = 0; base < m && !s_stop; base += kScanWin) {
+    // 1-2: filter and compact (key order: index u * kScanThreads + t)
+    unsigned long long key[kScanPer];
+    bool fr[kScanPer];
 #pragma unroll
-    for (int u = 0; u < CPT; u++) {
+    for (int u = 0; u < kScanPer; u++) {
       key[u] = nxt[u];
-      const int64_t i2 = base + WIN + (int64_t)t * CPT + u;  // prefetch the next window
+      const int64_t i2 = base + kScanWin + (int64_t)u * kScanThreads + t;  // prefetch the next window
       nxt[u] = i2 < m ? sorted[i2] : 0ull;
-      acc[u] = false;
-      und[u] = false;
-      jb[u][0] = jb[u][1] = jb[u][2] = 0;
-      if (key[u]) {
-        const int64_t sid = (int64_t)(0xFFFFFFFFull - (key[u] & 0xFFFFFFFFull));
-        int64_t j[3];
-        unrank_set<NS>(sid, j);
-        und[u] = true;
-#pragma unroll
-        for (int q = 0; q < NS; q++) {
-          jb[u][q] = (int32_t)j[q];
-          und[u] = und[u] && !((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u);
-        }
-      }
+      int32_t jb[3];
+      fr[u] = key[u] != 0ull && key_jobs_free<NS>(fmt, key[u], s_taken, jb);
     }
-    // rounds: every undecided key claims its jobs with a round-stamped
-    // atomicMax of (round << 12 | 4095 - index); a key that holds the claim on
-    // all its jobs is the lowest undecided key on each of them, so the
-    // sequential rule takes it. Stamps grow with the round, so the claims of
-    // earlier rounds never need resetting: two barriers per round.
-    bool any = false;
+    unsigned bm[kScanPer];
 #pragma unroll
-    for (int u = 0; u < CPT; u++) any = any || und[u];
-    if (__syncthreads_or(any)) {
-      bool cont = true;
-      while (cont) {
-        const unsigned stamp = rnd << 12;
+    for (int u = 0; u < kScanPer; u++) {
+      bm[u] = __ballot_sync(0xFFFFFFFFu, fr[u]);
+      if (lane == 0) s_cnt[u * kScanWarps + wid] = __popc(bm[u]);
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive prefix over the (u, warp) counts in key order; a lane owns consecutive ones
+      int c[kCntPerLane], sum = 0;
 #pragma unroll
-        for (int u = 0; u < CPT; u++)
-          if (und[u])
+      for (int r = 0; r < kCntPerLane; r++) {
+        c[r] = s_cnt[lane * kCntPerLane + r];
+        sum += c[r];
+      }
+      int incl = sum;
 #pragma unroll
-            for (int q = 0; q < NS; q++) atomicMax(&s_first[jb[u][q]], stamp | (unsigned)(WIN - 1 - (t * CPT + u)));
-        __syncthreads();
-        bool left = false;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
 #pragma unroll
-        for (int u = 0; u < CPT; u++) {
-          if (!und[u]) continue;
-          const unsigned mine = stamp | (unsigned)(WIN - 1 - (t * CPT + u));
-          bool take = true;
+      for (int r = 0; r < kCntPerLane; r++) {
+        s_cnt[lane * kCntPerLane + r] = run;
+        run += c[r];
+      }
+      if (lane == 31) s_n = incl;
+    }
+    __syncthreads();
 #pragma unroll
-          for (int q = 0; q < NS; q++) take = take && (s_first[jb[u][q]] == mine);
-          if (take) {
+    for (int u = 0; u < kScanPer; u++)
+      if (fr[u]) s_surv[s_cnt[u * kScanWarps + wid] + __popc(bm[u] & ((1u << lane) - 1u))] = key[u];
+    __syncthreads();
+    const int off = s_n;
+    // 3: warp 0 resolves the survivors in order, kRes groups of 32 per step: all
+    // their shared-memory loads in flight at once (the step is latency-bound);
+    // a pick removes the keys sharing a job from its own and the later groups
+    if (wid == 0) {
+      constexpr int kRes = 8;
+      for (int g = 0; g < off && np < k_max; g += 32 * kRes) {
+        unsigned long long kk[kRes];
+        int32_t jb[kRes][3];
+        unsigned cand[kRes];
 #pragma unroll
-            for (int q = 0; q < NS; q++) atomicOr(&s_taken[jb[u][q] >> 5], 1u << (jb[u][q] & 31));
-            acc[u] = true;
-            und[u] = false;
-          }
-          left = left || und[u];
+        for (int r = 0; r < kRes; r++) {
+          const int e = g + 32 * r + lane;
+          kk[r] = e < off ? s_surv[e] : 0ull;
+          jb[r][0] = jb[r][1] = jb[r][2] = -1;
+          const bool ok = kk[r] != 0ull && key_jobs_free<NS>(fmt, kk[r], s_taken, jb[r]);
+          cand[r] = __ballot_sync(0xFFFFFFFFu, ok);
         }
-        rnd++;
-        cont = __syncthreads_or(left);  // every taken bit of this round is visible after it
-        if (cont) {
 #pragma unroll
-          for (int u = 0; u < CPT; u++)
-            if (und[u])
+        for (int r = 0; r < kRes; r++) {
+          while (cand[r] && np < k_max) {
+            const int l = __ffs(cand[r]) - 1;
+            int32_t tj[3];
+#pragma unroll
+            for (int q = 0; q < NS; q++) tj[q] = __shfl_sync(0xFFFFFFFFu, jb[r][q], l);
+            const unsigned long long pk = __shfl_sync(0xFFFFFFFFu, kk[r], l);
+            if (lane == 0) {
+#pragma unroll
+              for (int q = 0; q < NS; q++) s_taken[tj[q] >> 5] |= 1u << (tj[q] & 31);
+              picks[np] = gkey_canonical<NS>(fmt, pk, tj);
+            }
+            np++;
+#pragma unroll
+            for (int r2 = 0; r2 < kRes; r2++) {
+              if (r2 < r) continue;
+              bool clash = false;
 #pragma unroll
               for (int q = 0; q < NS; q++)
-                if ((s_taken[jb[u][q] >> 5] >> (jb[u][q] & 31)) & 1u) und[u] = false;
+#pragma unroll
+                for (int q2 = 0; q2 < NS; q2++) clash = clash || (jb[r2][q] == tj[q2]);
+              cand[r2] &= ~__ballot_sync(0xFFFFFFFFu, clash);
+            }
+            __syncwarp();
+          }
         }
       }
+      if (lane == 0) s_stop = np >= k_max;
     }
-    // emit the window's picks in index order (block prefix sum), stopping at k_max
-    int cnt = 0;
-#pragma unroll
-    for (int u = 0; u < CPT; u++) cnt += acc[u];
-    int incl = cnt;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-      if ((t & 31) >= off) incl += v;
-    }
-    if ((t & 31) == 31) s_wsum[t >> 5] = incl;
-    __syncthreads();
-    if (t < 32) {
-      int v = s_wsum[t];
-      for (int off = 1; off < 32; off <<= 1) {
-        const int u2 = __shfl_up_sync(0xFFFFFFFFu, v, off);
-        if (t >= off) v += u2;
-      }
-      s_wsum[t] = v;  // inclusive over warps
-    }
-    __syncthreads();
-    const int64_t np0 = s_np;
-    int rank = (t >= 32 ? s_wsum[(t >> 5) - 1] : 0) + incl - cnt;
-#pragma unroll
-    for (int u = 0; u < CPT; u++)
-      if (acc[u]) {
-        if (np0 + rank < k_max) picks[np0 + rank] = key[u];
-        rank++;
-      }
-    __syncthreads();
-    if (t == 0) s_np = (np0 + s_wsum[31] < k_max) ? np0 + s_wsum[31] : k_max;
-    __syncthreads();
+    __syncthreads();  // taken bits and the stop flag are visible to the next window
   }
-  for (int i = threadIdx.x; i < words; i += blockDim.x) taken_g[i] = s_taken[i];
-  if (threadIdx.x == 0) *n_picks = s_np;
+  for (int i = t; i < words; i += kScanThreads) taken_g[i] = s_taken[i];
+  if (t == 0) *n_picks = np;
 }
 
 // predicate of the order-preserving re-filter between scan chunks
 template <int NS>
 struct AllJobsFree {
   const uint32_t* bits;
+  GKeyFmt fmt;
   __device__ __forceinline__ bool operator()(const unsigned long long& key) const {
     if (!key) return false;
-    const int64_t sid = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
-    int64_t j[3];
-    unrank_set<NS>(sid, j);
-    bool fr = true;
-#pragma unroll
-    for (int q = 0; q < NS; q++) fr = fr && !((bits[j[q] >> 5] >> (j[q] & 31)) & 1u);
-    return fr;
+    int32_t jb[3];
+    return key_jobs_free<NS>(fmt, key, bits, jb);
   }
 };
 
 size_t select_temp_bytes(int64_t n) {
   size_t bytes = 0;
-  AllJobsFree<2> pred{nullptr};
+  AllJobsFree<2> pred{nullptr, GKeyFmt()};
   cub::DeviceSelect::If((void*)nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
                         (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), pred);
   size_t b3 = 0;
-  AllJobsFree<3> pred3{nullptr};
+  AllJobsFree<3> pred3{nullptr, GKeyFmt()};
   cub::DeviceSelect::If((void*)nullptr, b3, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
                         (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), pred3);
   return std::max(bytes, b3);
@@ -446,10 +521,10 @@ size_t select_temp_bytes(int64_t n) {
 
 cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const unsigned long long* in,
                              unsigned long long* out, int64_t* n_out, int64_t n, const uint32_t* taken_bits,
-                             cudaStream_t st) {
+                             const GKeyFmt& fmt, cudaStream_t st) {
   if (n_slots == 2)
-    return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<2>{taken_bits}, st);
-  return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<3>{taken_bits}, st);
+    return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<2>{taken_bits, fmt}, st);
+  return cub::DeviceSelect::If(temp, temp_bytes, in, out, n_out, (int)n, AllJobsFree<3>{taken_bits, fmt}, st);
 }
 
 // ---- launchers -------------------------------------------------------------------------
@@ -466,16 +541,16 @@ void launch_obj_hist(const float* obj, int64_t count, const unsigned* mm, int nb
 }
 void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
-                          unsigned long long* n_keys, cudaStream_t st) {
+                          unsigned long long* n_keys, const GKeyFmt& fmt, cudaStream_t st) {
   if (count <= 0) return;
   int64_t blocks = std::min<int64_t>((count + 32 * kKirWarps * 4 * kKirLoads - 1) / (32 * kKirWarps * 4 * kKirLoads),
                                      148 * 8);
   if (n_slots == 2)
     k_keys_in_range<2><<<(unsigned)blocks, 32 * kKirWarps, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi,
-                                                                    taken_bits, keys, n_keys);
+                                                                    taken_bits, keys, n_keys, fmt);
   else
     k_keys_in_range<3><<<(unsigned)blocks, 32 * kKirWarps, 0, st>>>(obj, first, count, mm, nbins, bin_lo, bin_hi,
-                                                                    taken_bits, keys, n_keys);
+                                                                    taken_bits, keys, n_keys, fmt);
 }
 
 size_t sort_temp_bytes(int64_t n) {
@@ -486,20 +561,25 @@ size_t sort_temp_bytes(int64_t n) {
 }
 
 cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
-                           int64_t n, cudaStream_t st) {
-  return cub::DeviceRadixSort::SortKeysDescending(temp, temp_bytes, in, out, (int)n, 0, 64, st);
+                           int64_t n, cudaStream_t st, int end_bit) {
+  return cub::DeviceRadixSort::SortKeysDescending(temp, temp_bytes, in, out, (int)n, 0, end_bit, st);
 }
 
-cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
-                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
-                               cudaStream_t st) {
-  const size_t smem = (size_t)((n_jobs + 31) / 32) * 4 + (size_t)n_jobs * 4;
+cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, const int64_t* m_dev,
+                               int64_t n_jobs, uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks,
+                               int64_t k_max, const GKeyFmt& fmt, cudaStream_t st, int64_t* scanned) {
+  // dynamic shared memory: a window's survivors (64 KB) and the taken bitmask
+  // (n_jobs bits; <= 2^20 jobs, far above any queue the set scorer accepts)
+  const size_t smem = sizeof(unsigned long long) * kScanWin + (size_t)((n_jobs + 31) / 32) * 4;
+  if (n_jobs > ((int64_t)1 << 20)) return cudaErrorInvalidValue;
   if (n_slots == 2) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_greedy_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_greedy_scan<2><<<1, 1024, smem, st>>>(sorted, m, n_jobs, taken_bits, picks, n_picks, k_max);
+    cudaError_t e = smem_optin((const void*)k_greedy_scan<2>, smem);
+    if (e != cudaSuccess) return e;
+    k_greedy_scan<2><<<1, kScanThreads, smem, st>>>(sorted, m, m_dev, n_jobs, taken_bits, picks, n_picks, k_max, fmt, scanned);
   } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_greedy_scan<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_greedy_scan<3><<<1, 1024, smem, st>>>(sorted, m, n_jobs, taken_bits, picks, n_picks, k_max);
+    cudaError_t e = smem_optin((const void*)k_greedy_scan<3>, smem);
+    if (e != cudaSuccess) return e;
+    k_greedy_scan<3><<<1, kScanThreads, smem, st>>>(sorted, m, m_dev, n_jobs, taken_bits, picks, n_picks, k_max, fmt, scanned);
   }
   return cudaGetLastError();
 }
