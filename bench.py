@@ -346,6 +346,25 @@ def calibration_metrics(pb, F, dev, args):
     pipeline["evaluate_ms"] = e0.elapsed_time(e1)
     pipeline["note"] = ("C, D fitted on the synthetic GPU; the fitted table searched over the queue; proposals "
                         "scored by the ground truth (PAPER.md L752/L777 analogue)")
+    # hill climbing (NEXT #2) on the calibrated table: its decisions against the
+    # exhaustive search on the same table, and its proposals scored by the ground truth
+    obj_e, cfg_e = sf.score_all(Fd)
+    obj_e, cfg_e = obj_e.clone(), cfg_e.clone()
+    hill = {}
+    balanced = int(np.argmin(np.asarray(pb.state_gpcs).max(axis=1)))
+    for name, start in (("first_state_pmax", (0, pb.n_caps - 1)), ("balanced_pmax", (balanced, pb.n_caps - 1))):
+        sf.set_search(1, *start)
+        obj_h, cfg_h = sf.score_all(Fd)
+        evals = sf.last_search_evals()
+        feas = (cfg_e >= 0) & (cfg_h >= 0)
+        ratio = obj_h[feas].double() / obj_e[feas].double()
+        _, hs = sf.evaluate_truth(Fd, truth)
+        hill[name] = {"same_config_as_exhaustive": float((cfg_h == cfg_e).double().mean().item()),
+                      "objective_ratio_geomean": float(torch.exp(torch.log(ratio).mean()).item()) if ratio.numel() else None,
+                      "evals_per_set": evals / max(cfg_e.numel(), 1),
+                      "truth_geomean_prop_over_best": hs["geomean_prop_over_best"]}
+        sf.set_search(0)
+    pipeline["hill_climb_on_calibrated_table"] = hill
     sf.close()
     n_solo, n_co = len(ts.solo_app), len(ts.co_app)
     npart = ts.co_partners.shape[1] if n_co else 0

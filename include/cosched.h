@@ -109,6 +109,19 @@ const char* cosched_last_error(cosched_t h);
 /* Message for errors that happen before a handle exists (create). */
 const char* cosched_last_create_error(void);
 
+/* ---- Limits (all checked; a call outside them returns the status named) ----
+ *  - sets per queue <= 2^32 - 2 (set ids are 32-bit in the argmax keys):
+ *    pairs up to 92,682 jobs, triples up to 2,954 jobs        -> COSCHED_E_ARG
+ *  - n_slots 1..3, n_states <= 128, n_caps <= 64, n_slices <= 32767 (create) -> COSCHED_E_ARG
+ *  - greedy allocation: queues up to 2^20 jobs (the taken bitmask of the
+ *    one-block scan lives in shared memory; every queue the scorer accepts
+ *    fits); per-rank batches below 2^30 keys (CUB int counts), chosen by the
+ *    library                                                    -> COSCHED_E_CUDA
+ *  - exact allocation: k * n_slots == n_jobs with n_jobs <= 20 (pairs) / 15 (triples)
+ *  - node budgeting: integer-watt caps, node_power_w / gcd(caps) <= 12287 -> COSCHED_E_ARG
+ *  - the tiled pair scorer covers every queue the set limit allows (fewer than
+ *    32768 column tiles); shards are whole colex columns by construction. */
+
 /* ---- multi-GPU (one process per GPU) -------------------------------------
  * The search shards by contiguous set-id range (whole colex columns, i.e. a
  * range of the largest job position) with no data-path exchange; the only

@@ -302,12 +302,16 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   // forces the locally-dominant-rounds fallback of the multi-rank greedy
   int64_t cap_max = (int64_t)16 << 20;
   if (const char* e = getenv("COSCHED_GREEDY_BATCH_CAP")) cap_max = std::max<int64_t>(1, atoll(e));
+  // CUB's sort / select take int item counts: a gathered batch (cap x nranks) stays below 2^30
+  cap_max = std::min<int64_t>(cap_max, ((int64_t)1 << 30) / std::max(nranks, 1));
   const int64_t cap = nranks > 0 ? std::min<int64_t>(largest, cap_max) : n_sets_local;
   w.batch_cap = cap;
   const int64_t gathered = nranks > 0 ? cap * nranks : 0;
   w.gath = (unsigned long long*)take((size_t)gathered * 8 + 8);
   w.gath_sorted = (unsigned long long*)take((size_t)gathered * 8 + 8);
-  const int64_t list_max = std::max<int64_t>(nranks > 0 ? gathered : n_sets_local, 1);
+  // the longest list a sort / select sees: a batch (<= 64 M keys, greedy_sorted_scan) or a
+  // gathered batch -- never the whole shard, which may exceed CUB's int item counts
+  const int64_t list_max = std::max<int64_t>(std::min<int64_t>(nranks > 0 ? gathered : n_sets_local, (int64_t)1 << 30), 1);
   w.sort_tmp_bytes = std::max(sort_temp_bytes(list_max), select_temp_bytes(list_max));
   w.sort_tmp = take(w.sort_tmp_bytes);
   // exact re-scoring list of the tiled scorers: normally empty; an

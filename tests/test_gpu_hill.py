@@ -71,7 +71,7 @@ def _parity(cs, pb, F, start, jobs=None, min_exact=0.999):
     m = same & (cfg_o >= 0)
     assert np.all(np.abs(obj_g[m] - obj_o[m]) <= TAU_OBJ * np.abs(obj_o[m]))
     n = F.shape[0] if jobs is None else len(jobs)
-    for sid in np.nonzero(~same)[0][:200]:
+    for sid in np.nonzero(~same)[0]:  # every disagreement is a valid climb outcome
         rows = [F[p] if jobs is None else F[jobs[p]] for p in oracle.unrank(n, pb.n_slots, int(sid))]
         assert _valid_local_optimum(o, pb, rows, int(cfg_g[sid]), float(obj_g[sid])), sid
     # the ABI reports the total evaluation count: it equals the oracle's when every path matched
