@@ -319,6 +319,9 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   // memory bound, not a correctness one
   int64_t rcap = (int64_t)1 << 20;
   if (const char* e = getenv("COSCHED_RESCORE_CAP")) rcap = std::max<int64_t>(0, atoll(e));  // testing knob: overflow path
+  w.pipe_ring = (unsigned long long*)take(greedy_pipe_ring_bytes());
+  w.pipe_cnt = (int*)take(sizeof(int) * kPipeSlots);
+  w.pipe_ctl = (int*)take(sizeof(int) * (kPipeSlots + 4));
   w.rescore_cap = (unsigned)std::min<int64_t>(std::max<int64_t>(n_sets_local, 1), rcap);
   w.rescore_list = (unsigned*)take((size_t)std::max<unsigned>(w.rescore_cap, 1u) * 4);
   // the pair scorer's stage-split tail: at most one CTA-slot round of tiles
@@ -1059,6 +1062,25 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     }
     CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s, fmt.end_bit));
     h->launches++;
+    if (getenv("COSCHED_GREEDY_PIPE") && atoi(getenv("COSCHED_GREEDY_PIPE")) != 0) {
+      // (COSCHED_GREEDY_PIPE=1, measured slower on C4: DESIGN.md §5) the whole sorted
+      // batch through the producer / consumer pipeline (one cooperative launch)
+      CK(launch_greedy_pipe(ns, sorted, m, N, taken_bits, ws.picked, np_dev, k, fmt, ws.pipe_ring, ws.pipe_cnt,
+                            ws.pipe_ctl, ws.pipe_ctl + kPipeSlots, s));
+      h->launches += 2;
+      h->greedy_rounds++;
+      CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (getenv("COSCHED_GREEDY_STATS")) {
+        int surv = 0;
+        CK(cudaMemcpy(&surv, ws.pipe_ctl + kPipeSlots + 3, 4, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "greedy pipe batch: %lld keys, %d survivors to the consumer, %lld picks\n", (long long)m, surv,
+                (long long)n_picks);
+      }
+      bin_hi = bin_lo - 1;
+      kBatch = std::min<int64_t>(kBatchMax, kBatch * 2);
+      continue;
+    }
     // scan the sorted list in windows of kWin keys: the first window as it is
     // (its keys were free at the batch start), every later window after an
     // order-preserving select of the keys still free (a full-GPU pass over that

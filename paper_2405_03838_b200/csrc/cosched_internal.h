@@ -115,6 +115,9 @@ struct Workspace {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   int64_t batch_cap = 0;                   // keys per rank per greedy batch
+  unsigned long long* pipe_ring = nullptr; // greedy pipeline ring (greedy_pipe_ring_bytes)
+  int* pipe_cnt = nullptr;                 // [kPipeSlots]
+  int* pipe_ctl = nullptr;                 // [kPipeSlots + 4] ring flags, then next / done / stop
   unsigned long long* merge = nullptr;     // [merge_tiles][64 * 64] (PairMerge)
   int64_t merge_tiles = 0;
   unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
@@ -156,6 +159,15 @@ cudaError_t select_free_keys(int n_slots, void* temp, size_t temp_bytes, const u
                              const GKeyFmt& fmt, cudaStream_t st);
 cudaError_t sort_keys_desc(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out,
                            int64_t n, cudaStream_t st, int end_bit = 64);
+// The sequential rule over a sorted list as a whole-GPU producer / consumer
+// pipeline (one cooperative launch); ring / ring_cnt / pipe_ctl from the workspace
+// (pipe_ctl: kPipeLag ring flags then 4 control words, reset by the launch).
+cudaError_t launch_greedy_pipe(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
+                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
+                               const GKeyFmt& fmt, unsigned long long* ring, int* ring_cnt, int* ring_flag, int* ctl,
+                               cudaStream_t st);
+size_t greedy_pipe_ring_bytes();
+constexpr int kPipeSlots = 16;  // = kPipeLag in greedy.cu
 // picks are written as canonical packed keys (cosched_pack_key); the list length is
 // *m_dev when m_dev != NULL (a count produced on the device), else m
 cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, const int64_t* m_dev,

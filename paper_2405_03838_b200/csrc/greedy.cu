@@ -495,6 +495,259 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   if (t == 0) *n_picks = np;
 }
 
+// ---- the sequential rule as a producer / consumer pipeline over the whole GPU ----
+// One cooperative launch per sorted batch (all CTAs resident, one per SM).
+// Producers (CTAs 1..G-1) claim windows of kPipeWin consecutive keys of the
+// sorted list in order, drop the keys with a taken job -- reading the taken
+// bitmask the consumer publishes, at most kPipeLag windows stale -- and write
+// the survivors, still in key order, to a ring slot. The consumer (warp 0 of
+// CTA 0) takes the slots in window order and applies the sequential rule to
+// the survivors against its own exact taken bitmask (shared memory): a
+// survivor whose jobs are all free is the next pick. Staleness only lets
+// extra keys through the filter; the picks are exactly the sequential
+// greedy's. The consumer publishes every pick's jobs (global taken bits) and
+// its window progress; producers wait when kPipeLag windows ahead.
+#ifndef COSCHED_PIPE_PARTS
+#define COSCHED_PIPE_PARTS 2
+#endif
+#ifndef COSCHED_PIPE_AHEAD
+#define COSCHED_PIPE_AHEAD 4
+#endif
+constexpr int kPipeThreads = 512, kPipePer = 16, kPipeSub = kPipeThreads * kPipePer, kPipeParts = COSCHED_PIPE_PARTS;
+constexpr int kPipeWin = kPipeSub * kPipeParts, kPipeLag = kPipeSlots;
+constexpr int kPipeAhead = COSCHED_PIPE_AHEAD;  // producers run at most this many windows ahead of the consumer
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    k_greedy_pipe(const unsigned long long* __restrict__ sorted, int64_t m, int64_t n_jobs, uint32_t* taken_g,
+                  unsigned long long* picks, int64_t* n_picks, int64_t k_max, const GKeyFmt fmt,
+                  unsigned long long* ring, int* ring_cnt, int* ring_flag, int* ctl /* [0] next, [1] done, [2] stop */) {
+  extern __shared__ __align__(16) unsigned long long p_dyn[];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t n_win = (m + kPipeWin - 1) / kPipeWin;
+  const int words = (int)((n_jobs + 31) >> 5);
+  if (blockIdx.x == 0) {
+    // ---------------- consumer ----------------
+    // warps 1..: loaders -- wait for window w+1's slot and copy its survivors into
+    // the shared buffer (w+1) % 2; warp 0: the sequential rule over buffer w % 2,
+    // against the exact taken bitmask in shared memory. One barrier per window.
+    constexpr int kBuf = kPipeSub;  // survivors staged per window; beyond that warp 0 reads the slot in L2
+    unsigned long long* s_buf = p_dyn;                                        // [2][kBuf]
+    uint32_t* s_taken = reinterpret_cast<uint32_t*>(p_dyn + 2 * kBuf);       // n_jobs bits
+    __shared__ int s_c[2], s_stop_c;
+    for (int i = t; i < words; i += kPipeThreads) s_taken[i] = taken_g[i];
+    if (t == 0) s_stop_c = 0;
+    constexpr int kLoaders = kPipeThreads - 32;
+    auto load = [&](int64_t w) {  // loader warps only
+      const int slot = (int)(w % kPipeLag);
+      if (t == 32)
+        while (ld_acquire(ring_flag + slot) != (int)(w + 1)) __nanosleep(32);
+      asm volatile("bar.sync 1, %0;" ::"r"(kLoaders));  // loaders only
+      const int c = __ldcg(ring_cnt + slot);
+      const unsigned long long* src = ring + (size_t)slot * kPipeWin;
+      unsigned long long* dst = s_buf + (size_t)(w & 1) * kBuf;
+      const int cs = c < kBuf ? c : kBuf;
+      for (int e = t - 32; e < cs; e += kLoaders) dst[e] = __ldcg(src + e);
+      if (t == 32) {
+        s_c[w & 1] = c;
+        atomicAdd(ctl + 3, c);  // survivors (instrumentation)
+      }
+    };
+    if (t >= 32 && n_win > 0) load(0);
+    __syncthreads();
+    int64_t np = *n_picks;
+    for (int64_t w = 0; w < n_win; w++) {
+      if (wid == 0) {
+        const int c = s_c[w & 1];
+        const unsigned long long* sv = s_buf + (size_t)(w & 1) * kBuf;
+        const unsigned long long* gv = ring + (size_t)(w % kPipeLag) * kPipeWin;
+        constexpr int kRes = 8;
+        for (int g = 0; g < c && np < k_max; g += 32 * kRes) {
+          unsigned long long kk[kRes];
+          int32_t jb[kRes][3];
+          unsigned cand[kRes];
+#pragma unroll
+          for (int r = 0; r < kRes; r++) {
+            const int e = g + 32 * r + lane;
+            kk[r] = e < c ? (e < kBuf ? sv[e] : __ldcg(gv + e)) : 0ull;
+            jb[r][0] = jb[r][1] = jb[r][2] = -1;
+            const bool ok = kk[r] != 0ull && key_jobs_free<NS>(fmt, kk[r], s_taken, jb[r]);
+            cand[r] = __ballot_sync(0xFFFFFFFFu, ok);
+          }
+#pragma unroll
+          for (int r = 0; r < kRes; r++) {
+            while (cand[r] && np < k_max) {
+              const int l = __ffs(cand[r]) - 1;
+              int32_t tj[3];
+#pragma unroll
+              for (int q = 0; q < NS; q++) tj[q] = __shfl_sync(0xFFFFFFFFu, jb[r][q], l);
+              const unsigned long long pk = __shfl_sync(0xFFFFFFFFu, kk[r], l);
+              if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < NS; q++) {
+                  s_taken[tj[q] >> 5] |= 1u << (tj[q] & 31);
+                  atomicOr(taken_g + (tj[q] >> 5), 1u << (tj[q] & 31));  // published to the producers
+                }
+                picks[np] = gkey_canonical<NS>(fmt, pk, tj);
+              }
+              np++;
+#pragma unroll
+              for (int r2 = 0; r2 < kRes; r2++) {
+                if (r2 < r) continue;
+                bool clash = false;
+#pragma unroll
+                for (int q = 0; q < NS; q++)
+#pragma unroll
+                  for (int q2 = 0; q2 < NS; q2++) clash = clash || (jb[r2][q] == tj[q2]);
+                cand[r2] &= ~__ballot_sync(0xFFFFFFFFu, clash);
+              }
+              __syncwarp();
+            }
+          }
+        }
+        if (lane == 0 && np >= k_max) s_stop_c = 1;
+      } else if (w + 1 < n_win) {
+        load(w + 1);
+      }
+      __syncthreads();
+      if (t == 0) st_release(ctl + 1, (int)(w + 1));  // window w consumed: its ring slot is free
+      if (s_stop_c) break;
+    }
+    if (t == 0) {
+      *n_picks = np;
+      st_release(ctl + 2, 1);  // stop: the producers exit
+    }
+    return;
+  }
+  // ---------------- producers ----------------
+  __shared__ int s_w, s_stop;
+  __shared__ int s_cnt[kPipePer * (kPipeThreads / 32)];
+  __shared__ int s_n;
+  constexpr int kWarps = kPipeThreads / 32, kCntPerLane = kPipePer * kWarps / 32;
+  for (;;) {
+    if (t == 0) {
+      int w = atomicAdd(ctl + 0, 1);
+      int stop = ld_acquire(ctl + 2);
+      while (!stop && w < n_win && w >= ld_acquire(ctl + 1) + kPipeAhead) {
+        __nanosleep(128);
+        stop = ld_acquire(ctl + 2);
+      }
+      s_w = w;
+      s_stop = stop;
+    }
+    __syncthreads();
+    const int64_t w = s_w;
+    if (s_stop || w >= n_win) return;
+    const int slot = (int)(w % kPipeLag);
+    unsigned long long* dst = ring + (size_t)slot * kPipeWin;
+    int run = 0;  // survivors written so far (block-uniform)
+    for (int part = 0; part < kPipeParts; part++) {
+    const int64_t base = w * kPipeWin + (int64_t)part * kPipeSub;
+    unsigned long long key[kPipePer];
+    bool fr[kPipePer];
+#pragma unroll
+    for (int u = 0; u < kPipePer; u++) {
+      const int64_t i = base + (int64_t)u * kPipeThreads + t;
+      key[u] = i < m ? __ldg(sorted + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kPipePer; u++) {
+      fr[u] = false;
+      if (key[u]) {
+        int32_t jb[3];
+        gkey_jobs<NS>(fmt, key[u], jb);
+        bool f = true;
+#pragma unroll
+        for (int q = 0; q < NS; q++) f = f && !((ld_relaxed_u32(taken_g + (jb[q] >> 5)) >> (jb[q] & 31)) & 1u);
+        fr[u] = f;
+      }
+    }
+    unsigned bm[kPipePer];
+#pragma unroll
+    for (int u = 0; u < kPipePer; u++) {
+      bm[u] = __ballot_sync(0xFFFFFFFFu, fr[u]);
+      if (lane == 0) s_cnt[u * kWarps + wid] = __popc(bm[u]);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int c[kCntPerLane], sum = 0;
+#pragma unroll
+      for (int r = 0; r < kCntPerLane; r++) {
+        c[r] = s_cnt[lane * kCntPerLane + r];
+        sum += c[r];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int r = 0; r < kCntPerLane; r++) {
+        s_cnt[lane * kCntPerLane + r] = run;
+        run += c[r];
+      }
+      if (lane == 31) s_n = incl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPipePer; u++)
+      if (fr[u]) __stcg(dst + run + s_cnt[u * kWarps + wid] + __popc(bm[u] & ((1u << lane) - 1u)), key[u]);
+    run += s_n;
+    __syncthreads();  // s_cnt / s_n are rewritten by the next part
+    }
+    __syncthreads();  // every survivor written before the slot is published
+    if (t == 0) {
+      ring_cnt[slot] = run;
+      __threadfence();
+      st_release(ring_flag + slot, (int)(w + 1));
+    }
+  }
+}
+
+// One cooperative launch (all CTAs co-resident: the pipeline spin-waits across CTAs).
+cudaError_t launch_greedy_pipe(int n_slots, const unsigned long long* sorted, int64_t m, int64_t n_jobs,
+                               uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
+                               const GKeyFmt& fmt, unsigned long long* ring, int* ring_cnt, int* ring_flag, int* ctl,
+                               cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  if (n_jobs > ((int64_t)1 << 20)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(ring_flag, 0, sizeof(int) * (kPipeLag + 4), st);  // flags and ctl are contiguous
+  if (e != cudaSuccess) return e;
+  // consumer: two survivor buffers + the taken bitmask (the producers use none of it)
+  const size_t smem = sizeof(unsigned long long) * 2 * kPipeSub + (size_t)((n_jobs + 31) / 32) * 4;
+  const void* fn = n_slots == 2 ? (const void*)k_greedy_pipe<2> : (const void*)k_greedy_pipe<3>;
+  e = smem_optin(fn, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, n_slots == 2 ? (const void*)k_greedy_pipe<2>
+                                                                       : (const void*)k_greedy_pipe<3>,
+                                                kPipeThreads, smem);
+  const int64_t windows = (m + kPipeWin - 1) / kPipeWin;
+  int grid = (int)std::min<int64_t>((int64_t)num_sms() * std::max(per_sm, 1), windows + 1);
+  grid = std::max(grid, 2);
+  void* args[] = {(void*)&sorted, (void*)&m, (void*)&n_jobs, (void*)&taken_bits, (void*)&picks, (void*)&n_picks,
+                  (void*)&k_max, (void*)&fmt, (void*)&ring, (void*)&ring_cnt, (void*)&ring_flag, (void*)&ctl};
+  return cudaLaunchCooperativeKernel(fn, grid, kPipeThreads, args, smem, st);
+}
+
+size_t greedy_pipe_ring_bytes() { return sizeof(unsigned long long) * kPipeWin * kPipeLag; }
+
 // predicate of the order-preserving re-filter between scan chunks
 template <int NS>
 struct AllJobsFree {
