@@ -1032,9 +1032,16 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       unsigned long long width;
       bin_range_ord(mmh[0], mmh[1], bin_lo, bin_hi, &u_lo, &width);
       fmt = gkey_format(ns, N, u_lo, width);
-      launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
-                           (unsigned long long*)ws.alive, nk_dev, fmt, s);
-      h->launches++;
+      // once a quarter of the jobs is taken, read only the live rows (free j1, or free j1 < j2)
+      if (n_free * 4 <= N * 3) {
+        launch_keys_live(ns, taken_bits, N, (int32_t*)ws.job_key, ws.counters + 5, n_free, h->out_obj, h->first,
+                         h->n_sets, ws.mm, bin_lo, bin_hi, (unsigned long long*)ws.alive, nk_dev, fmt, s);
+        h->launches += 2;
+      } else {
+        launch_keys_in_range(ns, h->out_obj, h->first, h->n_sets, ws.mm, kHistBins, bin_lo, bin_hi, taken_bits,
+                             (unsigned long long*)ws.alive, nk_dev, fmt, s);
+        h->launches++;
+      }
     }
     int64_t nk = 0;
     CK(cudaMemcpyAsync(&nk, nk_dev, 8, cudaMemcpyDeviceToHost, s));

@@ -146,6 +146,11 @@ GKeyFmt gkey_format(int n_slots, int64_t n_jobs, unsigned base, unsigned long lo
 void launch_keys_in_range(int n_slots, const float* obj, int64_t first, int64_t count, const unsigned* mm, int nbins,
                           int bin_lo, int bin_hi, const uint32_t* taken_bits, unsigned long long* keys,
                           unsigned long long* n_keys, const GKeyFmt& fmt, cudaStream_t st);
+// The same keys from the live rows only (free j1 / free pairs j1 < j2, over the free list it builds)
+void launch_keys_live(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
+                      int64_t n_free, const float* obj, int64_t first, int64_t count, const unsigned* mm, int bin_lo,
+                      int bin_hi, unsigned long long* keys, unsigned long long* n_keys, const GKeyFmt& fmt,
+                      cudaStream_t st);
 // [lo ord, hi ord) of histogram bins [bin_lo, bin_hi] given the objective range mm = (lo, hi)
 void bin_range_ord(unsigned lo, unsigned hi, int bin_lo, int bin_hi, unsigned* u_lo, unsigned long long* width);
 // greedy endgame: keys of every feasible set of free jobs (free list built on the device)

@@ -182,11 +182,16 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   // one 32-bit unsigned compare: u_lo <= hi < 2^32 and u_hi - u_lo <= span + 1 < 2^32;
   // -inf (infeasible) has ord 0x007FFFFF < lo <= u_lo, so it wraps to a large value
   const unsigned r_lo = (unsigned)u_lo, r_w = (unsigned)(u_hi - u_lo);
+  // on raw float bits: every feasible objective is > 0 (Fairness > alpha >= 0
+  // makes every RPerf, hence Throughput, positive), so the range lies in the
+  // positive floats, where ord(o) = bits(o) | 2^31; the infeasible -inf
+  // (0xFF800000) lands far above the range after the subtraction
+  const unsigned b_lo = r_lo & 0x7FFFFFFFu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int64_t* qid = s_id[wib];
   float* qo = s_o[wib];
   int qn = 0;  // warp-uniform queue length
-  auto in_range = [&](float o) { return ord_float_d(o) - r_lo < r_w; };
+  auto in_range = [&](float o) { return __float_as_uint(o) - b_lo < r_w; };
   unsigned long long* ob = s_out[wib];
   int on = 0;  // warp-uniform output buffer length
   auto flush = [&]() {
@@ -261,6 +266,93 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_in_range(const float* _
   }
   if (qn > 0) drain(qn);
   flush();
+}
+
+__global__ void k_free_list(const uint32_t* __restrict__ taken_bits, int64_t n_jobs, int32_t* __restrict__ free_list,
+                            int64_t* __restrict__ n_free);
+
+// The range pass restricted to live rows: once many jobs are taken, only the
+// sets whose two largest jobs are free can be picked, and for fixed (j1, j2)
+// (pairs: j1) the sets j0 < j1 are one contiguous run of the objective array.
+// A warp walks such runs -- rows enumerated over the ascending free-job list,
+// pairs: every free j1, triples: every free pair j1 < j2 -- reads only their
+// objectives and emits the in-range keys whose j0 is free too. The data read
+// falls with the square (triples: cube) of the free fraction.
+template <int NS>
+__global__ void __launch_bounds__(32 * kKirWarps) k_keys_live(const int32_t* __restrict__ free_list, int64_t n_rows,
+                                                             const float* __restrict__ obj, int64_t first,
+                                                             int64_t count, const unsigned* __restrict__ mm,
+                                                             int bin_lo, int bin_hi,
+                                                             const uint32_t* __restrict__ taken_bits,
+                                                             unsigned long long* keys, unsigned long long* n_keys,
+                                                             const GKeyFmt fmt) {
+  __shared__ unsigned long long s_out[kKirWarps][kKirOut];
+  const unsigned lo = mm[0], span = mm[1] - mm[0];
+  const unsigned long long u_lo = bin_start(lo, span, bin_lo), u_hi = bin_start(lo, span, bin_hi + 1);
+  const unsigned b_lo = (unsigned)u_lo & 0x7FFFFFFFu, r_w = (unsigned)(u_hi - u_lo);  // raw-bits test (k_keys_in_range)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned long long* ob = s_out[wib];
+  int on = 0;
+  auto flush = [&]() {
+    if (on == 0) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(n_keys, (unsigned long long)on);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int e = lane; e < on; e += 32) keys[base + e] = ob[e];
+    __syncwarp();
+    on = 0;
+  };
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n_rows; r += nw) {
+    int64_t j[3];
+    int64_t s0;  // set id of (j0 = 0, j1, j2)
+    if (NS == 2) {
+      j[1] = free_list[r];
+      s0 = c2(j[1]);
+    } else {
+      int64_t ab[2];
+      unrank_set<2>(r, ab);  // the r-th free pair, ascending positions in the free list
+      j[1] = free_list[ab[0]];
+      j[2] = free_list[ab[1]];
+      s0 = c3(j[2]) + c2(j[1]);
+    }
+    const int64_t lo_i = s0 > first ? s0 : first, hi_i = s0 + j[1] < first + count ? s0 + j[1] : first + count;
+    for (int64_t base = lo_i; base < hi_i; base += 32) {  // warp-uniform
+      const int64_t sid = base + lane;
+      bool ok = false;
+      unsigned long long kk = 0ull;
+      if (sid < hi_i) {
+        const float o = __ldcs(obj + (sid - first));
+        j[0] = sid - s0;
+        if (__float_as_uint(o) - b_lo < r_w && !((__ldg(taken_bits + (j[0] >> 5)) >> (j[0] & 31)) & 1u)) {
+          ok = true;
+          kk = gkey_make<NS>(fmt, o, sid, j);
+        }
+      }
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+      if (ok) ob[on + __popc(m & ((1u << lane) - 1u))] = kk;
+      on += __popc(m);
+      __syncwarp();
+      if (on > kKirOut - 32) flush();
+    }
+  }
+  flush();
+}
+
+void launch_keys_live(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, int32_t* free_list, int64_t* n_free_dev,
+                      int64_t n_free, const float* obj, int64_t first, int64_t count, const unsigned* mm, int bin_lo,
+                      int bin_hi, unsigned long long* keys, unsigned long long* n_keys, const GKeyFmt& fmt,
+                      cudaStream_t st) {
+  k_free_list<<<1, 1024, 0, st>>>(taken_bits, n_jobs, free_list, n_free_dev);
+  const int64_t rows = n_slots == 2 ? n_free : n_free * (n_free - 1) / 2;
+  if (rows <= 0 || count <= 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>((rows + kKirWarps - 1) / kKirWarps, 148 * 8);
+  if (n_slots == 2)
+    k_keys_live<2><<<blocks, 32 * kKirWarps, 0, st>>>(free_list, rows, obj, first, count, mm, bin_lo, bin_hi,
+                                                      taken_bits, keys, n_keys, fmt);
+  else
+    k_keys_live<3><<<blocks, 32 * kKirWarps, 0, st>>>(free_list, rows, obj, first, count, mm, bin_lo, bin_hi,
+                                                      taken_bits, keys, n_keys, fmt);
 }
 
 // Endgame of the greedy: once few jobs are free, the sets that can still be
