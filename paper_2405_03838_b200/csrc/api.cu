@@ -1131,6 +1131,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     CK(cudaStreamSynchronize(s));
     fprintf(stderr, "greedy: %lld picks, %lld keys through the scan, %lld windows\n", (long long)n_picks,
             (long long)scanned, (long long)h->greedy_rounds);
+    scan_prof_report();
   }
   picks->resize(n_picks);
   if (n_picks) {

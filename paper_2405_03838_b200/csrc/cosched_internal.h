@@ -175,6 +175,7 @@ size_t greedy_pipe_ring_bytes();
 constexpr int kPipeSlots = 16;  // = kPipeLag in greedy.cu
 // picks are written as canonical packed keys (cosched_pack_key); the list length is
 // *m_dev when m_dev != NULL (a count produced on the device), else m
+void scan_prof_report();  // COSCHED_SCAN_PROF builds: print and reset the scan phase counters
 cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, const int64_t* m_dev,
                                int64_t n_jobs, uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks,
                                int64_t k_max, const GKeyFmt& fmt, cudaStream_t st, int64_t* scanned = nullptr);
@@ -228,6 +229,32 @@ bool tiled_applicable(int n_slots, int64_t n_jobs, int64_t first, int64_t count)
 // returns the CUDA error of the opt-in. num_sms(): SMs of the current device.
 cudaError_t smem_optin(const void* func, size_t bytes);
 int num_sms();
+
+// Programmatic dependent launch (PDL) along the step's kernel chain (validate ->
+// project -> gather -> scorer -> re-score -> best detail): a kernel launched with
+// launch_pdl may start while its predecessor on the stream drains; it runs its
+// prologue (constant tables into shared memory, barrier init) and then waits in
+// pdl_wait() until the predecessor has completed and its writes are visible.
+// Every such kernel calls pdl_wait() before touching anything an earlier kernel
+// of the stream writes, and pdl_launch_dependents() only after it (so at most
+// two adjacent kernels overlap). Both are no-ops for a normal launch.
+// COSCHED_PDL=0 turns the attribute off (A/B timing).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 // Step start: err = ~0 (valid), best_key = 0, rescore count = 0, wmm = empty ranges.
 void launch_step_init(unsigned long long* err, unsigned long long* best_key, unsigned* rescore_n, unsigned* wmm,
                       cudaStream_t st);

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "cosched_internal.h"
 #include "device_common.cuh"
@@ -451,6 +452,11 @@ void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, i
 // per-job state: any queue the set scorer accepts fits shared memory.
 constexpr int kScanThreads = 512, kScanPer = 4, kScanWin = kScanThreads * kScanPer, kScanWarps = kScanThreads / 32;
 
+#ifdef COSCHED_SCAN_PROF
+// instrumentation build only: [0] filter cycles, [1] resolution cycles, [2] chunks,
+// [3] survivors, [4] picks, [5] launches, [6] whole-kernel cycles
+__device__ unsigned long long g_scan_prof[8];
+#endif
 template <int NS>
 __device__ __forceinline__ bool key_jobs_free(const GKeyFmt& f, unsigned long long key, const uint32_t* bits,
                                               int32_t* jb) {
@@ -488,7 +494,14 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     nxt[u] = i < m ? sorted[i] : 0ull;
   }
   __syncthreads();
+#ifdef COSCHED_SCAN_PROF
+  const long long t_k0 = clock64();
+  long long t_f = 0, t_r = 0, n_ch = 0, n_sv = 0, np0 = np;
+#endif
   for (int64_t base = 0; base < m && !s_stop; base += kScanWin) {
+#ifdef COSCHED_SCAN_PROF
+    const long long t_c0 = clock64();
+#endif
     // 1-2: filter and compact (key order: index u * kScanThreads + t)
     unsigned long long key[kScanPer];
     bool fr[kScanPer];
@@ -534,6 +547,12 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       if (fr[u]) s_surv[s_cnt[u * kScanWarps + wid] + __popc(bm[u] & ((1u << lane) - 1u))] = key[u];
     __syncthreads();
     const int off = s_n;
+#ifdef COSCHED_SCAN_PROF
+    const long long t_c1 = clock64();
+    t_f += t_c1 - t_c0;
+    n_ch++;
+    n_sv += off;
+#endif
     // 3: warp 0 resolves the survivors in order, kRes groups of 32 per step: all
     // their shared-memory loads in flight at once (the step is latency-bound);
     // a pick removes the keys sharing a job from its own and the later groups
@@ -582,7 +601,21 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       if (lane == 0) s_stop = np >= k_max;
     }
     __syncthreads();  // taken bits and the stop flag are visible to the next window
+#ifdef COSCHED_SCAN_PROF
+    t_r += clock64() - t_c1;
+#endif
   }
+#ifdef COSCHED_SCAN_PROF
+  if (t == 0) {
+    atomicAdd(&g_scan_prof[0], (unsigned long long)t_f);
+    atomicAdd(&g_scan_prof[1], (unsigned long long)t_r);
+    atomicAdd(&g_scan_prof[2], (unsigned long long)n_ch);
+    atomicAdd(&g_scan_prof[3], (unsigned long long)n_sv);
+    atomicAdd(&g_scan_prof[5], 1ull);
+    atomicAdd(&g_scan_prof[6], (unsigned long long)(clock64() - t_k0));
+  }
+  if (t == 0) atomicAdd(&g_scan_prof[4], (unsigned long long)(np - np0));
+#endif
   for (int i = t; i < words; i += kScanThreads) taken_g[i] = s_taken[i];
   if (t == 0) *n_picks = np;
 }
@@ -929,4 +962,16 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
   return cudaGetLastError();
 }
 
+#ifdef COSCHED_SCAN_PROF
+void scan_prof_report() {
+  unsigned long long v[8];
+  cudaMemcpyFromSymbol(v, g_scan_prof, sizeof v);
+  fprintf(stderr, "scan prof: filter %.3f Mcyc, resolve %.3f Mcyc, kernel %.3f Mcyc, chunks %llu, survivors %llu, picks %llu, launches %llu\n",
+          v[0] / 1e6, v[1] / 1e6, v[6] / 1e6, v[2], v[3], v[4], v[5]);
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_scan_prof, z, sizeof z);
+}
+#else
+void scan_prof_report() {}
+#endif
 }  // namespace cosched

@@ -32,6 +32,8 @@ __global__ void k_validate(const float* __restrict__ F, int64_t n_rows, const in
                            int64_t n_jobs, unsigned long long* err, float* __restrict__ hj) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= n_jobs) return;
+  // the inputs were copied before the step began: read and test them before
+  // the PDL wait; the err word (reset by k_step_init) and hj after it
   int64_t row = jobs ? (int64_t)jobs[q] : q;
   int code = 0;
   if (row < 0 || row >= n_rows) {
@@ -52,20 +54,26 @@ __global__ void k_validate(const float* __restrict__ F, int64_t n_rows, const in
     if (!code) {
       float h[6], j[3];
       basis_hj(v, h, j);
+      pdl_wait();
+      pdl_launch_dependents();
       float4* o = reinterpret_cast<float4*>(hj + q * 12);
       o[0] = make_float4(h[0], h[1], h[2], h[3]);
       o[1] = make_float4(h[4], h[5], j[0], j[1]);
       o[2] = make_float4(j[2], 0.0f, 0.0f, 0.0f);
     }
   }
-  if (code) atomicMin(err, ((unsigned long long)q << 8) | (unsigned long long)code);
+  if (code) {
+    pdl_wait();
+    atomicMin(err, ((unsigned long long)q << 8) | (unsigned long long)code);
+  }
 }
 
 void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs, int64_t n_jobs,
                      unsigned long long* err, float* hj, cudaStream_t st) {
   if (n_jobs <= 0) return;
   int bs = 256;
-  k_validate<<<(unsigned)((n_jobs + bs - 1) / bs), bs, 0, st>>>(features, n_rows, jobs, n_jobs, err, hj);
+  launch_pdl(k_validate, dim3((unsigned)((n_jobs + bs - 1) / bs)), dim3(bs), 0, st, features, n_rows, jobs, n_jobs, err,
+             hj);
 }
 
 // ---------------------------------------------------------------------------
@@ -221,6 +229,8 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
   }
   if (threadIdx.x < 2) s_mm[threadIdx.x] = threadIdx.x ? 0u : 0xFFFFFFFFu;
   __syncthreads();
+  pdl_wait();  // hj, err and wmm of this step (the prologue above reads constant tables only)
+  pdl_launch_dependents();
   if (*err != ~0ull) return;  // invalid input: leave the workspace untouched (uniform per launch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rs = sp.rs, ld = rs + 1, nc = sp.n_caps;
@@ -319,11 +329,6 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   const int role = blockIdx.y / sp.n_stages, stage = blockIdx.y - role * sp.n_stages;
   const int slot = role / (NS + 1), kind = role % (NS + 1);  // 0 = A, NS = W, else B
   const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);  // real configs in this stage
-  if (threadIdx.x == 0) {
-    const float inv = quant_inv<NS>(wmm);
-    s_inv = inv;
-    s_nlo = -__fmul_rn(unord_float_d(wmm[2 * slot]), inv);
-  }
   if (threadIdx.x < ncol) {
     const int c = stage * kStageCfg + threadIdx.x, st = c / sp.n_caps, p = c - st * sp.n_caps;
     CoefRow r;
@@ -336,6 +341,13 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
       load_d(r.d[0], sp, coef_d, sp.slice[st][l], p);
     }
     s_coef[threadIdx.x] = r;
+  }
+  pdl_wait();  // the projection's w range (wmm), hj and err
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    const float inv = quant_inv<NS>(wmm);
+    s_inv = inv;
+    s_nlo = -__fmul_rn(unord_float_d(wmm[2 * slot]), inv);
   }
   __syncthreads();
   if (*err != ~0ull) return;
@@ -400,6 +412,14 @@ cudaError_t smem_optin(const void* func, size_t bytes) {
   return e;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("COSCHED_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -431,14 +451,14 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   smem_optin((const void*)k_project_all<2>, 72 * 1024);
   smem_optin((const void*)k_project_all<3>, 72 * 1024);
   if (sp.n_slots == 1) {
-    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    k_gather_fast<1><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+    launch_pdl(k_project_all<1>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_gather_fast<1>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else if (sp.n_slots == 2) {
-    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    k_gather_fast<2><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+    launch_pdl(k_project_all<2>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_gather_fast<2>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else {
-    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    k_gather_fast<3><<<gg, kProjJobs, 0, st>>>(hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
+    launch_pdl(k_project_all<3>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_gather_fast<3>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   }
 }
 
@@ -627,6 +647,8 @@ __global__ void __launch_bounds__(256) k_rescore_sets(const SpaceParams sp, cons
                                                       float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
                                                       unsigned long long* __restrict__ best_key, const RescoreBuf rb,
                                                       const unsigned long long* __restrict__ err) {
+  pdl_wait();  // the scorer's outputs and re-score list
+  pdl_launch_dependents();
   if (*err != ~0ull) return;
   const float thr = rescore_threshold<NS>(rb.wmm);
   const unsigned n_listed = *rb.n;
@@ -677,9 +699,9 @@ int launch_rescore(const SpaceParams& sp, const float* w, const float* fast, int
   // up to 8 resident blocks per SM: enough loads in flight for the scan mode
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (count + 1023) / 1024));
   if (sp.n_slots == 2)
-    k_rescore_sets<2><<<grid, 256, 0, st>>>(sp, fast, w, first, count, obj, cfg, best_key, rb, err);
+    launch_pdl(k_rescore_sets<2>, dim3(grid), dim3(256), 0, st, sp, fast, w, first, count, obj, cfg, best_key, rb, err);
   else
-    k_rescore_sets<3><<<grid, 256, 0, st>>>(sp, fast, w, first, count, obj, cfg, best_key, rb, err);
+    launch_pdl(k_rescore_sets<3>, dim3(grid), dim3(256), 0, st, sp, fast, w, first, count, obj, cfg, best_key, rb, err);
   return 1;
 }
 
@@ -810,6 +832,8 @@ __global__ void __launch_bounds__(256) k_sets_detail(const SpaceParams sp, const
                                                      const float* __restrict__ coef_d) {
   __shared__ unsigned long long s_key[32];
   __shared__ float s_hj[3 * 12];
+  pdl_wait();  // (launch_best_detail) the step's best key and outputs
+  pdl_launch_dependents();
   float* out = out_all + (int64_t)blockIdx.x * 8;
   int64_t set_id;
   if (set_ids) {
@@ -918,12 +942,14 @@ void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb,
   // host_out is pinned host memory (UVA-mapped): [0] validation word, [1] key,
   // [2..5] the detail row -- the kernel writes it directly, no copy. tb != NULL:
   // operands from hj and the coefficient tables (no ka / kb this step)
+  const int64_t* no_ids = nullptr;
+  const float* no_tab = nullptr;
   if (tb)
-    k_sets_detail<true><<<1, 256, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
-                                           host_out, hj, tb->coef_c, tb->coef_d);
+    launch_pdl(k_sets_detail<true>, dim3(1), dim3(256), 0, st, sp, ka, kb, w, no_ids, key,
+               reinterpret_cast<float*>(host_out + 2), err, host_out, hj, tb->coef_c, tb->coef_d);
   else
-    k_sets_detail<false><<<1, 256, 0, st>>>(sp, ka, kb, w, nullptr, key, reinterpret_cast<float*>(host_out + 2), err,
-                                            host_out, nullptr, nullptr, nullptr);
+    launch_pdl(k_sets_detail<false>, dim3(1), dim3(256), 0, st, sp, ka, kb, w, no_ids, key,
+               reinterpret_cast<float*>(host_out + 2), err, host_out, no_tab, no_tab, no_tab);
 }
 
 // Rank sort of a short list of unique keys, descending: position of key i =

@@ -140,7 +140,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ float s_thr;  // exact re-scoring threshold (rescore_threshold)
-  if (*err != ~0ull) return;
   constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
   constexpr int stage_floats = 6 * kTile * rs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -154,20 +153,25 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
   int64_t t = blockIdx.x;  // work unit
   if (t >= g.n_units) {
-    block_max_key(0ull, best_key);
+    pdl_wait();
+    if (*err == ~0ull) block_max_key(0ull, best_key);
     return;
   }
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_fence_init();
-    s_thr = rescore_threshold<2>(rb.wmm);
   }
   // per pair ([j1 local][j0 local], padded rows): state of the best masked key
   // (written when a state improves) and, at tile end, the key itself
   float* sbest = smem + 2 * stage_floats;
   int16_t* sbg = reinterpret_cast<int16_t*>(sbest + kTile * kBgRow);
   for (int e = threadIdx.x; e < kTile * kBgRow; e += kThreads) sbg[e] = -1;
+  // the prologue above touches shared memory only: it overlaps the gather's tail (PDL)
+  pdl_wait();
+  pdl_launch_dependents();
+  if (*err != ~0ull) return;  // uniform
+  if (threadIdx.x == 0) s_thr = rescore_threshold<2>(rb.wmm);
   __syncthreads();
   int64_t I, J;
   int b0, s_lo, s_hi;  // stages [s_lo, s_hi) of the unit (the whole config axis unless SPLIT)
@@ -534,9 +538,11 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     g.n_seg = 0;
     const int64_t grid = n_whole < slots ? n_whole : slots;
     if (minb == 1)
-      k_score_pairs_tiled<1, 4, false><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+      launch_pdl(k_score_pairs_tiled<1, 4, false>, dim3((unsigned)grid), dim3(kThreads), smem, st, sp, g, w, fast, obj,
+                 cfg, best_key, err, rb);
     else
-      k_score_pairs_tiled<2, 4, false><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+      launch_pdl(k_score_pairs_tiled<2, 4, false>, dim3((unsigned)grid), dim3(kThreads), smem, st, sp, g, w, fast, obj,
+                 cfg, best_key, err, rb);
   }
   if (n_sg > 1) {
     launches += 3;

@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(kTThreads, MINB)
                           unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
-  if (*err != ~0ull) return;
   constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
   constexpr int stage_floats = 8 * kTT * rs + 4 * rs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -206,7 +205,8 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   for (int e = threadIdx.x; e < kTT * kTBgRow; e += kTThreads) sbg[e] = -1;
   int64_t t = blockIdx.x;
   if (t >= g.n_tiles) {
-    block_max_key(0ull, best_key);
+    pdl_wait();
+    if (*err == ~0ull) block_max_key(0ull, best_key);
     return;
   }
   if (threadIdx.x == 0) {
@@ -214,6 +214,10 @@ __global__ void __launch_bounds__(kTThreads, MINB)
     mbar_init(&bars[1], 1);
     mbar_fence_init();
   }
+  // the prologue touches shared memory only: it overlaps the gather's tail (PDL)
+  pdl_wait();
+  pdl_launch_dependents();
+  if (*err != ~0ull) return;  // uniform
   __syncthreads();
   int64_t J2, B, A;
   ttile_coords(g, t, &J2, &B, &A);
@@ -318,8 +322,27 @@ __global__ void __launch_bounds__(kTThreads, MINB)
           const float bo = bc >= 0 ? __fadd_rn(f0[u], __fadd_rn(f1[u], f2[u])) : -INFINITY;
           const int64_t sid = sid2 + (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
           const int64_t k = sid - g.first_set;
+#ifdef COSCHED_L2HINT_ST
+          // this tile's run of row (j1, j2) is [k0, k0 + len); a 32-byte sector that
+          // also holds outputs of a neighbouring run is written in two parts, often
+          // a whole round apart: keep it in L2 (evict_last) until both parts land,
+          // so it is never evicted half-written (a DRAM read-modify-write)
+          const int64_t k0 = sid2 + (((int64_t)j1 * (j1 - 1)) >> 1) + jA - g.first_set;
+          const int len = min(kTT, j1 - jA);
+          const int64_t ka = k + (int64_t)((((uintptr_t)out_obj) >> 2) & 7);  // sector-relative index
+          const int64_t ka0 = k0 + (int64_t)((((uintptr_t)out_obj) >> 2) & 7);
+          const bool shared_sector = ((ka & ~7ll) < ka0) || ((ka | 7ll) >= ka0 + len);
+#ifdef COSCHED_L2HINT_NORMAL
+          const uint64_t pol = shared_sector ? l2_evict_last() : l2_evict_normal();
+#else
+          const uint64_t pol = shared_sector ? l2_evict_last() : l2_evict_first();
+#endif
+          if (out_obj) st_l2hint(out_obj + k, bo, pol);
+          if (out_cfg) st_l2hint(out_cfg + k, bc, pol);
+#else
           if (out_obj) out_obj[k] = bo;
           if (out_cfg) out_cfg[k] = bc;
+#endif
           if (bc >= 0) {
             const unsigned long long kk = pack_key(bo, sid);
             key = kk > key ? kk : key;
@@ -387,9 +410,11 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
   if (grid > g.n_tiles) grid = g.n_tiles;
   if (grid < 1) grid = 1;
   if (minb == 1)
-    k_score_triples_tiled<1><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+    launch_pdl(k_score_triples_tiled<1>, dim3((unsigned)grid), dim3(kTThreads), smem, st, sp, g, w, fast, obj, cfg,
+               best_key, err);
   else
-    k_score_triples_tiled<2><<<(unsigned)grid, kTThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err);
+    launch_pdl(k_score_triples_tiled<2>, dim3((unsigned)grid), dim3(kTThreads), smem, st, sp, g, w, fast, obj, cfg,
+               best_key, err);
   return 1;
 }
 
