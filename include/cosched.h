@@ -216,6 +216,16 @@ cosched_status cosched_local_best_key(cosched_t h, uint64_t* key);
  * COSCHED_INFEASIBLE if no set has a feasible config. */
 cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj);
 
+/* cosched_best_set in two halves. _begin enqueues the same work on the stream
+ * of the last score_all (the all-reduce when a communicator is set, then the
+ * detail kernel, which writes the result into the handle's pinned host buffer)
+ * and returns without synchronising, so the caller can record an event after
+ * the step's last device work; _end synchronises that stream and returns what
+ * cosched_best_set returns. Every _begin must be followed by one _end before
+ * the next call on the handle; _end without _begin returns COSCHED_E_STATE. */
+cosched_status cosched_best_set_begin(cosched_t h);
+cosched_status cosched_best_set_end(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj);
+
 /* The best config of one set of the last scored queue, evaluated on the GPU
  * (any rank, any set, no comm). rperf: host float[n_slots] (may be NULL);
  * throughput / fairness / obj: host (may be NULL). COSCHED_INFEASIBLE (cfg -1)

@@ -221,6 +221,18 @@ class Scheduler:
                          allow_infeasible=True)
         return st, sid.value, cfg.value, obj.value
 
+    def best_set_begin(self):
+        """Enqueue best_set's device work on the last score_all's stream; no synchronisation
+        (record an event after it to time the step's device work), then call best_set_end."""
+        self._check(self._L.cosched_best_set_begin(self._h))
+
+    def best_set_end(self):
+        """Synchronise and return best_set's (status, set_id, cfg, obj)."""
+        sid, cfg, obj = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_float()
+        st = self._check(self._L.cosched_best_set_end(self._h, ctypes.byref(sid), ctypes.byref(cfg),
+                                                      ctypes.byref(obj)), allow_infeasible=True)
+        return st, sid.value, cfg.value, obj.value
+
     def best_config(self, set_id: int) -> dict:
         cfg, obj, thr, fair = ctypes.c_int32(), ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
         rp = (ctypes.c_float * 3)()

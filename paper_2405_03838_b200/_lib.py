@@ -88,6 +88,8 @@ SIGNATURES = [
     ("cosched_score_all", I32, [P, P, I64, P, I64, P, ctypes.c_size_t, ctypes.POINTER(Out), P]),
     ("cosched_local_best_key", I32, [P, P]),
     ("cosched_best_set", I32, [P, P, P, P]),
+    ("cosched_best_set_begin", I32, [P]),
+    ("cosched_best_set_end", I32, [P, P, P, P]),
     ("cosched_best_config", I32, [P, I64, P, P, P, P, P]),
     ("cosched_best_allocation", I32, [P, I32, P, P, P, P]),
     ("cosched_set_variant", I32, [P, ctypes.c_int]),

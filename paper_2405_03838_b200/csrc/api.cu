@@ -116,7 +116,8 @@ struct cosched_ctx {
   unsigned long long* h_pinned = nullptr;  // [8] pinned host readback
   // last score_all
   bool scored = false;
-  bool kakb_valid = false;  // ka / kb rows of this step's projection present (else launch_project_kakb on demand)
+  bool kakb_valid = false;
+  bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called  // ka / kb rows of this step's projection present (else launch_project_kakb on demand)
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
   Workspace ws{};
@@ -130,7 +131,8 @@ struct cosched_ctx {
   int64_t greedy_rounds = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t side = nullptr;                 // partial-column units of the pair scorer (PairMerge)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr;                // its stage-split tail units
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   // host copies of the table (ground-truth evaluation)
   std::vector<int32_t> h_gpcs, h_mem;
   std::vector<float> h_caps;
@@ -328,6 +330,7 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   // (2 resident CTAs per SM), 32 KB each (pairs only)
   w.merge_tiles = n_slots == 2 ? 2 * (int64_t)num_sms() : 0;
   w.merge = (unsigned long long*)take((size_t)w.merge_tiles * 64 * 64 * 8);
+  w.merge_cnt = (unsigned*)take((size_t)std::max<int64_t>(w.merge_tiles, 1) * 4);  // finished units per split tile
   w.rescore_n = (unsigned*)take(8);
   w.bytes = off;
   if (ws) *ws = w;
@@ -489,8 +492,10 @@ cosched_status cosched_create(const cosched_desc* d, int cuda_device, cosched_t*
             cudaEventCreate(&h->ev[0]) == cudaSuccess && cudaEventCreate(&h->ev[1]) == cudaSuccess &&
             cudaEventCreate(&h->ev[2]) == cudaSuccess && cudaEventCreate(&h->ev[3]) == cudaSuccess &&
             cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
             cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->ev_join2, cudaEventDisableTiming) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_c, d->coef_c, nc * 6 * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
             cudaMemcpy(h->tb.coef_d, d->coef_d, nc * 3 * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) {
@@ -521,7 +526,9 @@ void cosched_destroy(cosched_t h) {
       if (h->ev[i]) cudaEventDestroy(h->ev[i]);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->ev_join2) cudaEventDestroy(h->ev_join2);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->side2) cudaStreamDestroy(h->side2);
   }
   delete h;
 }
@@ -791,8 +798,11 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     pm.buf = ws.merge;
     pm.tiles = ws.merge_tiles;
     pm.side = h->side;
+    pm.side2 = h->side2;
+    pm.cnt = ws.merge_cnt;
     pm.ev_fork = h->ev_fork;
     pm.ev_join = h->ev_join;
+    pm.ev_join2 = h->ev_join2;
     h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
                                 ws.err, h->variant, st, rb, pm);
   }
@@ -878,8 +888,8 @@ static cosched_status detail_rows(cosched_t h, const int64_t* ids, int64_t n, st
   return COSCHED_OK;
 }
 
-cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj) {
-  NvtxRange nvtx_("cosched_best_set");
+cosched_status cosched_best_set_begin(cosched_t h) {
+  NvtxRange nvtx_("cosched_best_set_begin");
   if (!h) return COSCHED_E_ARG;
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
   DeviceGuard g(h->device);
@@ -892,8 +902,18 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->ws.err, h->h_pinned, h->ws.hj,
                      h->kakb_valid ? nullptr : &h->tb, h->stream);
   h->launches++;
+  h->best_pending = true;
+  return COSCHED_OK;
+}
+
+cosched_status cosched_best_set_end(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj) {
+  NvtxRange nvtx_("cosched_best_set_end");
+  if (!h) return COSCHED_E_ARG;
+  if (!h->best_pending) return fail(h, COSCHED_E_STATE, "cosched_best_set_end without cosched_best_set_begin");
+  h->best_pending = false;
+  DeviceGuard g(h->device);
   CK(cudaStreamSynchronize(h->stream));
-  st = deferred_status(h, h->h_pinned[0]);
+  cosched_status st = deferred_status(h, h->h_pinned[0]);
   if (st != COSCHED_OK) return st;
   const uint64_t key = h->h_pinned[1];
   float o;
@@ -909,6 +929,13 @@ cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, floa
   if (cfg) memcpy(cfg, h->h_pinned + 2, 4);
   if (obj) memcpy(obj, reinterpret_cast<const float*>(h->h_pinned + 2) + 1, 4);
   return COSCHED_OK;
+}
+
+cosched_status cosched_best_set(cosched_t h, int64_t* set_id, int32_t* cfg, float* obj) {
+  NvtxRange nvtx_("cosched_best_set");
+  cosched_status st = cosched_best_set_begin(h);
+  if (st != COSCHED_OK) return st;
+  return cosched_best_set_end(h, set_id, cfg, obj);
 }
 
 cosched_status cosched_best_config(cosched_t h, int64_t set_id, int32_t* cfg, float* obj, float* rperf,

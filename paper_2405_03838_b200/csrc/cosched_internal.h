@@ -74,12 +74,14 @@ struct RescoreBuf {
 // per pair of up to `tiles` 64 x 64 tiles.
 struct PairMerge {
   unsigned long long* buf = nullptr;
+  unsigned* cnt = nullptr;  // per split tile: stage-group units done (the last one resolves the tile)
   int64_t tiles = 0;
-  // the handle's side stream: the partial-column units run on it concurrently
-  // with the whole-tile and stage-split launches (forked after the gather,
-  // joined before the re-scoring pass); null = everything on the caller's stream
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the handle's side streams: the partial-column units (side) and the
+  // stage-split tail units (side2) run concurrently with the whole-tile launch,
+  // taking the CTA slots it frees (forked after the gather, joined before the
+  // re-scoring pass); null = everything on the caller's stream
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
 };
 
 // Device-side tables owned by a handle.
@@ -120,6 +122,7 @@ struct Workspace {
   int* pipe_ctl = nullptr;                 // [kPipeSlots + 4] ring flags, then next / done / stop
   unsigned long long* merge = nullptr;     // [merge_tiles][64 * 64] (PairMerge)
   int64_t merge_tiles = 0;
+  unsigned* merge_cnt = nullptr;            // [merge_tiles]: stage-group units done per split tile
   unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
   unsigned* rescore_n = nullptr;           // [1]
   unsigned rescore_cap = 0;

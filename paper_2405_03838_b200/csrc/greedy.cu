@@ -455,8 +455,31 @@ constexpr int kScanThreads = 512, kScanPer = 4, kScanWin = kScanThreads * kScanP
 #ifdef COSCHED_SCAN_PROF
 // instrumentation build only: [0] filter cycles, [1] resolution cycles, [2] chunks,
 // [3] survivors, [4] picks, [5] launches, [6] whole-kernel cycles
-__device__ unsigned long long g_scan_prof[8];
+__device__ unsigned long long g_scan_prof[12];
 #endif
+// a set's jobs in one word (jobs < 2^20, the scan's limit): j0 | j1 << 20 | j2 << 40
+template <int NS>
+__device__ __forceinline__ unsigned long long jobs_pack(const int32_t* jb) {
+  unsigned long long v = (unsigned long long)(uint32_t)jb[0];
+  if (NS > 1) v |= (unsigned long long)(uint32_t)jb[1] << 20;
+  if (NS > 2) v |= (unsigned long long)(uint32_t)jb[2] << 40;
+  return v;
+}
+template <int NS>
+__device__ __forceinline__ void jobs_unpack(unsigned long long v, int32_t* jb) {
+#pragma unroll
+  for (int q = 0; q < NS; q++) jb[q] = (int32_t)((v >> (20 * q)) & 0xFFFFFu);
+}
+template <int NS>
+__device__ __forceinline__ bool jobs_packed_free(unsigned long long v, const uint32_t* bits) {
+  bool fr = true;
+#pragma unroll
+  for (int q = 0; q < NS; q++) {
+    const unsigned j = (unsigned)((v >> (20 * q)) & 0xFFFFFu);
+    fr = fr && !((bits[j >> 5] >> (j & 31)) & 1u);
+  }
+  return fr;
+}
 template <int NS>
 __device__ __forceinline__ bool key_jobs_free(const GKeyFmt& f, unsigned long long key, const uint32_t* bits,
                                               int32_t* jb) {
@@ -478,7 +501,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   if (scanned && threadIdx.x == 0) atomicAdd((unsigned long long*)scanned, (unsigned long long)m);
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   unsigned long long* s_surv = s_dyn;                          // [kScanWin] survivors of a window
-  uint32_t* s_taken = reinterpret_cast<uint32_t*>(s_dyn + kScanWin);  // n_jobs bits
+  unsigned long long* s_sj = s_dyn + kScanWin;                 // [kScanWin] their jobs (jobs_pack)
+  uint32_t* s_taken = reinterpret_cast<uint32_t*>(s_dyn + 2 * kScanWin);  // n_jobs bits
+  __shared__ long long s_np;                                   // picks so far (every resolving warp starts from it)
+  __shared__ int s_pidx[kScanWin];                             // survivor index of each pick of a chunk
   __shared__ int s_cnt[kScanPer * (kScanThreads / 32)];
   constexpr int kCntPerLane = kScanPer * (kScanThreads / 32) / 32;  // the prefix pass: counts per lane of warp 0
   __shared__ int s_n;
@@ -486,7 +512,10 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   const int words = (int)((n_jobs + 31) >> 5);
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   for (int i = t; i < words; i += kScanThreads) s_taken[i] = taken_g[i];
-  if (t == 0) s_stop = 0;
+  if (t == 0) {
+    s_stop = 0;
+    s_np = np;
+  }
   unsigned long long nxt[kScanPer];
 #pragma unroll
   for (int u = 0; u < kScanPer; u++) {
@@ -503,15 +532,16 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     const long long t_c0 = clock64();
 #endif
     // 1-2: filter and compact (key order: index u * kScanThreads + t)
-    unsigned long long key[kScanPer];
+    unsigned long long key[kScanPer], jp[kScanPer];
     bool fr[kScanPer];
 #pragma unroll
     for (int u = 0; u < kScanPer; u++) {
       key[u] = nxt[u];
       const int64_t i2 = base + kScanWin + (int64_t)u * kScanThreads + t;  // prefetch the next window
       nxt[u] = i2 < m ? sorted[i2] : 0ull;
-      int32_t jb[3];
+      int32_t jb[3] = {0, 0, 0};
       fr[u] = key[u] != 0ull && key_jobs_free<NS>(fmt, key[u], s_taken, jb);
+      jp[u] = jobs_pack<NS>(jb);
     }
     unsigned bm[kScanPer];
 #pragma unroll
@@ -544,7 +574,11 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kScanPer; u++)
-      if (fr[u]) s_surv[s_cnt[u * kScanWarps + wid] + __popc(bm[u] & ((1u << lane) - 1u))] = key[u];
+      if (fr[u]) {
+        const int at = s_cnt[u * kScanWarps + wid] + __popc(bm[u] & ((1u << lane) - 1u));
+        s_surv[at] = key[u];
+        s_sj[at] = jp[u];
+      }
     __syncthreads();
     const int off = s_n;
 #ifdef COSCHED_SCAN_PROF
@@ -553,6 +587,90 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     n_ch++;
     n_sv += off;
 #endif
+#ifndef COSCHED_SCAN_OLD
+    // 3: the sequential rule over the chunk's survivors (all free at the chunk's
+    // start, in key order), by warp 0 in batches of 32 x 16: lane l holds
+    // survivors l + 32u (u < 16; jobs in registers, a live mask). Each step the
+    // smallest live index (one warp min) is the next pick -- every earlier
+    // survivor was picked or shares a job with a pick -- and every lane drops its
+    // survivors sharing a job with it (branch-free compares): one step per pick,
+    // whatever the number of survivors the pick blocks. Between batches the
+    // batch's picks are marked taken; the canonical keys are written after the
+    // chunk by the whole block.
+    np = s_np;  // warps that sat out earlier chunks catch up
+    const long long np0 = np;
+    if (wid == 0) {
+      constexpr int kLs = 16;  // survivors per lane and batch
+      for (int b0 = 0; b0 < off && np < k_max; b0 += 32 * kLs) {
+        unsigned long long jr[kLs];
+        unsigned live = 0u;
+#pragma unroll
+        for (int u = 0; u < kLs; u++) {
+          const int e = b0 + lane + 32 * u;
+          jr[u] = e < off ? s_sj[e] : 0ull;
+          if (e < off && jobs_packed_free<NS>(jr[u], s_taken)) live |= 1u << u;  // taken by earlier batches?
+        }
+        const long long npb = np;
+#ifdef COSCHED_SCAN_PROF
+        const long long t_l0 = clock64();
+        long long n_it = 0;
+#endif
+        while (np < k_max) {
+#ifdef COSCHED_SCAN_PROF
+          n_it++;
+#endif
+          const int my = live ? 32 * (__ffs(live) - 1) + lane : 0x7FFFFFFF;
+          const int g = __reduce_min_sync(0xFFFFFFFFu, my);
+          if (g == 0x7FFFFFFF) break;  // uniform: no live survivor left in the batch
+          const unsigned long long pj = s_sj[b0 + g];
+          const unsigned p0 = (unsigned)(pj & 0xFFFFFu), p1 = (unsigned)((pj >> 20) & 0xFFFFFu),
+                         p2 = (unsigned)((pj >> 40) & 0xFFFFFu);
+          unsigned kill = 0u;
+#pragma unroll
+          for (int u = 0; u < kLs; u++) {  // the pick itself too
+            bool c = false;
+#pragma unroll
+            for (int q = 0; q < NS; q++) {
+              const unsigned x = (unsigned)((jr[u] >> (20 * q)) & 0xFFFFFu);
+              c = c | (x == p0) | (NS > 1 && x == p1) | (NS > 2 && x == p2);
+            }
+            kill |= c ? (1u << u) : 0u;
+          }
+          live &= ~kill;
+          if (lane == 0) s_pidx[np - np0] = b0 + g;
+          np++;
+        }
+#ifdef COSCHED_SCAN_PROF
+        if (lane == 0) {
+          atomicAdd(&g_scan_prof[8], (unsigned long long)(clock64() - t_l0));
+          atomicAdd(&g_scan_prof[9], (unsigned long long)n_it);
+          atomicAdd(&g_scan_prof[10], 1ull);
+        }
+#endif
+        __syncwarp();
+        for (long long i = npb + lane; i < np; i += 32) {  // this batch's picks: taken for the next batches
+          int32_t tj[3];
+          jobs_unpack<NS>(s_sj[s_pidx[i - np0]], tj);
+#pragma unroll
+          for (int q = 0; q < NS; q++) atomicOr(&s_taken[tj[q] >> 5], 1u << (tj[q] & 31));
+        }
+        __syncwarp();
+      }
+    }
+    if (t == 0) s_np = np;
+    __syncthreads();
+    {
+      const long long np1 = s_np;
+      for (int i = t; i < (int)(np1 - np0); i += kScanThreads) {  // the chunk's picks, in parallel
+        const int g = s_pidx[i];
+        int32_t tj[3];
+        jobs_unpack<NS>(s_sj[g], tj);
+        picks[np0 + i] = gkey_canonical<NS>(fmt, s_surv[g], tj);
+      }
+      np = np1;
+      if (t == 0) s_stop = np1 >= k_max;
+    }
+#else
     // 3: warp 0 resolves the survivors in order, kRes groups of 32 per step: all
     // their shared-memory loads in flight at once (the step is latency-bound);
     // a pick removes the keys sharing a job from its own and the later groups
@@ -600,6 +718,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       }
       if (lane == 0) s_stop = np >= k_max;
     }
+#endif
     __syncthreads();  // taken bits and the stop flag are visible to the next window
 #ifdef COSCHED_SCAN_PROF
     t_r += clock64() - t_c1;
@@ -948,7 +1067,7 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
                                int64_t k_max, const GKeyFmt& fmt, cudaStream_t st, int64_t* scanned) {
   // dynamic shared memory: a window's survivors (64 KB) and the taken bitmask
   // (n_jobs bits; <= 2^20 jobs, far above any queue the set scorer accepts)
-  const size_t smem = sizeof(unsigned long long) * kScanWin + (size_t)((n_jobs + 31) / 32) * 4;
+  const size_t smem = sizeof(unsigned long long) * 2 * kScanWin + (size_t)((n_jobs + 31) / 32) * 4;
   if (n_jobs > ((int64_t)1 << 20)) return cudaErrorInvalidValue;
   if (n_slots == 2) {
     cudaError_t e = smem_optin((const void*)k_greedy_scan<2>, smem);
@@ -964,11 +1083,13 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
 
 #ifdef COSCHED_SCAN_PROF
 void scan_prof_report() {
-  unsigned long long v[8];
+  unsigned long long v[12];
   cudaMemcpyFromSymbol(v, g_scan_prof, sizeof v);
+  fprintf(stderr, "scan prof: pick loop %.3f Mcyc, %llu steps, %llu batches\n", v[8] / 1e6,
+          v[9], v[10]);
   fprintf(stderr, "scan prof: filter %.3f Mcyc, resolve %.3f Mcyc, kernel %.3f Mcyc, chunks %llu, survivors %llu, picks %llu, launches %llu\n",
           v[0] / 1e6, v[1] / 1e6, v[6] / 1e6, v[2], v[3], v[4], v[5]);
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbol(g_scan_prof, z, sizeof z);
 }
 #else

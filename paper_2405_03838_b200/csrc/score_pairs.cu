@@ -68,6 +68,7 @@ struct PairGrid {
   // as (key bits << 32 | ~stage) by atomicMax; k_pairs_merge_finish resolves them.
   int n_sg;
   unsigned long long* merge;
+  unsigned* cnt;  // non-null: per split tile, units done; the last unit resolves the tile (no finish launch)
 };
 
 __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_t* I, int64_t* J) {
@@ -130,6 +131,11 @@ __device__ __forceinline__ void issue_stage(float* stage, uint64_t* bar, const S
 
 }  // namespace
 
+__device__ __forceinline__ void merge_finish_part(const SpaceParams& sp, const PairGrid& g, const float* __restrict__ w,
+                                                  float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+                                                  const RescoreBuf& rb, unsigned long long* mg, int64_t I, int64_t J,
+                                                  int e0, float thr, unsigned long long* key);
+
 template <int MINB, int NB, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ float s_thr;  // exact re-scoring threshold (rescore_threshold)
+  __shared__ int s_last;   // SPLIT: this unit finished its tile
   constexpr int rs = kStageRS, rs4 = kStageRS / 4, chunks = kStageCfg / 4;
   constexpr int stage_floats = 6 * kTile * rs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -274,6 +281,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     ((unsigned long long)__float_as_uint(m) << 32) | (0xFFFFFFFFull - (unsigned long long)(unsigned)sbg[e]));
         sbg[e] = -1;
       }
+      if (g.cnt) {
+        // the tile's last unit to finish resolves it (threadfence reduction):
+        // every unit's merge atomics are visible before its count
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(g.cnt + (int)t / g.n_sg, 1u) == (unsigned)(g.n_sg - 1);
+        __syncthreads();
+        if (s_last) {
+          __threadfence();
+#pragma unroll 1
+          for (int q = 0; q < 4; q++)
+            merge_finish_part(sp, g, w, out_obj, out_cfg, rb, mg, I, J, q * (kTile * kTile / 4), s_thr, &key);
+          if (threadIdx.x == 0) g.cnt[(int)t / g.n_sg] = 0u;
+        }
+      }
     }
     if (!SPLIT && s == sp.n_stages - 1) {
       // ---- tile end: park each pair's best key, then resolve and write with a
@@ -366,27 +388,24 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // bits, as in the tile end -- and the exact FP32 objective w0 + w1 of it; the
 // merge entries are reset for the next step. Writes obj / cfg, the rescore flag
 // and the block's best key.
-__global__ void __launch_bounds__(256) k_pairs_merge_finish(const SpaceParams sp, const PairGrid g,
-                                                             const float* __restrict__ w, float* __restrict__ out_obj,
-                                                             int32_t* __restrict__ out_cfg,
-                                                             unsigned long long* __restrict__ best_key,
-                                                             const unsigned long long* __restrict__ err,
-                                                             const RescoreBuf rb) {
-  if (*err != ~0ull) return;
-  int64_t I, J;
-  tile_coords(g, g.t0 + blockIdx.x, &I, &J);
-  unsigned long long* mg = g.merge + (int64_t)blockIdx.x * (kTile * kTile);
-  const float thr = rescore_threshold<2>(rb.wmm);
+// Resolution of pairs [e0, e0 + 1024) of a stage-split tile (256 threads, 4
+// pairs each, all loads in flight): per pair the merged (best masked key, first
+// stage) gives the config -- stage and the key's low bits, as in the tile end --
+// and the exact FP32 objective w0 + w1 of it; the merge entries are reset for the
+// next step. Writes obj / cfg and the rescore flag; folds the best key into *key.
+__device__ __forceinline__ void merge_finish_part(const SpaceParams& sp, const PairGrid& g, const float* __restrict__ w,
+                                                  float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+                                                  const RescoreBuf& rb, unsigned long long* mg, int64_t I, int64_t J,
+                                                  int e0, float thr, unsigned long long* key) {
   const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
-  constexpr int kPer = 4;  // pairs per thread, all loads in flight; blockIdx.y: which quarter of the tile
+  constexpr int kPer = 4;
   int c_[kPer];
   float f0[kPer], f1[kPer];
-  const int e0 = blockIdx.y * (kTile * kTile / 4);
 #pragma unroll
   for (int u = 0; u < kPer; u++) {
     const int e = e0 + u * 256 + threadIdx.x, rj = e >> 6, ri = e & 63;
     const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
-    const unsigned long long v = mg[e];
+    const unsigned long long v = __ldcg(mg + e);  // L2: written by other CTAs' atomics
     mg[e] = 0ull;  // reset for the next step
     const bool ok = j0 < j1 && j1 >= g.c0 && j1 < g.c1;
     c_[u] = ok ? -1 : -2;
@@ -400,7 +419,6 @@ __global__ void __launch_bounds__(256) k_pairs_merge_finish(const SpaceParams sp
       f1[u] = __ldg(w + (int64_t)(w1base + st * npad + (int)j1) * rsz + p);
     }
   }
-  unsigned long long key = 0ull;
 #pragma unroll
   for (int u = 0; u < kPer; u++) {
     if (c_[u] == -2) continue;
@@ -413,13 +431,29 @@ __global__ void __launch_bounds__(256) k_pairs_merge_finish(const SpaceParams sp
     if (out_cfg) out_cfg[k] = c;
     if (c >= 0) {
       const unsigned long long kk = pack_key(bo, sid);
-      key = kk > key ? kk : key;
+      *key = kk > *key ? kk : *key;
       if (bo < thr) {
         const unsigned at = atomicAdd(rb.n, 1u);
         if (at < rb.cap) rb.list[at] = (unsigned)k;
       }
     }
   }
+}
+
+// Resolution of the stage-split tiles by a separate launch (four blocks per tile)
+// when the units do not resolve their tiles themselves (PairGrid::cnt null).
+__global__ void __launch_bounds__(256) k_pairs_merge_finish(const SpaceParams sp, const PairGrid g,
+                                                             const float* __restrict__ w, float* __restrict__ out_obj,
+                                                             int32_t* __restrict__ out_cfg,
+                                                             unsigned long long* __restrict__ best_key,
+                                                             const unsigned long long* __restrict__ err,
+                                                             const RescoreBuf rb) {
+  if (*err != ~0ull) return;
+  int64_t I, J;
+  tile_coords(g, g.t0 + blockIdx.x, &I, &J);
+  unsigned long long key = 0ull;
+  merge_finish_part(sp, g, w, out_obj, out_cfg, rb, g.merge + (int64_t)blockIdx.x * (kTile * kTile), I, J,
+                    blockIdx.y * (kTile * kTile / 4), rescore_threshold<2>(rb.wmm), &key);
   block_max_key(key, best_key);
 }
 
@@ -522,14 +556,24 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   }
   const int64_t n_whole = n_sg > 1 ? n_full - R : n_full;
   int launches = 0;
-  // partial-column units on the side stream: their CTAs take the slots the
-  // whole-tile launch frees in its last round, next to the stage-split units
-  const bool fork = n_seg > 0 && merge.side && merge.ev_fork && merge.ev_join;
-  cudaStream_t ust = st;
-  if (fork) {
-    cudaEventRecord(merge.ev_fork, st);
+  // partial-column units (side stream) and stage-split tail units (side2): both
+  // are enqueued at once next to the whole-tile launch, so their CTAs take the
+  // slots it frees in its last round (no launch gap); the tail units resolve
+  // their tiles themselves (last unit per tile, PairGrid::cnt).
+  // COSCHED_PAIR_TAIL_CONC=0: tail units and a finish launch on the caller's stream.
+  const char* tc = getenv("COSCHED_PAIR_TAIL_CONC");
+  const bool conc = n_sg > 1 && !(tc && tc[0] == '0') && merge.side2 && merge.cnt && merge.ev_join2 && merge.ev_fork;
+  const bool fork_side = n_seg > 0 && merge.side && merge.ev_fork && merge.ev_join;
+  g.cnt = nullptr;
+  if (fork_side || conc) cudaEventRecord(merge.ev_fork, st);
+  cudaStream_t ust = st, sst = st;
+  if (fork_side) {
     cudaStreamWaitEvent(merge.side, merge.ev_fork, 0);
     ust = merge.side;
+  }
+  if (conc) {
+    cudaStreamWaitEvent(merge.side2, merge.ev_fork, 0);
+    sst = merge.side2;
   }
   if (n_whole > 0) {
     launches++;
@@ -545,16 +589,19 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
                  cfg, best_key, err, rb);
   }
   if (n_sg > 1) {
-    launches += 3;
-    cudaMemsetAsync(merge.buf, 0, (size_t)R * kTile * kTile * sizeof(unsigned long long), st);
+    launches += conc ? 2 : 3;
+    cudaMemsetAsync(merge.buf, 0, (size_t)R * kTile * kTile * sizeof(unsigned long long), sst);
+    if (conc) cudaMemsetAsync(merge.cnt, 0, (size_t)R * sizeof(unsigned), sst);
     g.t0 = fa + n_whole;
     g.n_units = R * n_sg;
     g.n_sg = n_sg;
     g.merge = merge.buf;
+    g.cnt = conc ? merge.cnt : nullptr;
     g.n_seg = 0;
     const int64_t grid = g.n_units < slots ? g.n_units : slots;
-    k_score_pairs_tiled<2, 4, true><<<(unsigned)grid, kThreads, smem, st>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
-    k_pairs_merge_finish<<<dim3((unsigned)R, 4), 256, 0, st>>>(sp, g, w, obj, cfg, best_key, err, rb);
+    k_score_pairs_tiled<2, 4, true><<<(unsigned)grid, kThreads, smem, sst>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
+    if (!conc) k_pairs_merge_finish<<<dim3((unsigned)R, 4), 256, 0, st>>>(sp, g, w, obj, cfg, best_key, err, rb);
+    g.cnt = nullptr;
   }
   if (n_seg > 0) {
     launches++;
@@ -573,9 +620,13 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
     const int64_t grid = end < slots ? end : slots;
     k_score_pairs_tiled<2, 1, false><<<(unsigned)grid, kThreads, smem, ust>>>(sp, g, w, fast, obj, cfg, best_key, err, rb);
   }
-  if (fork) {
+  if (fork_side) {
     cudaEventRecord(merge.ev_join, merge.side);
     cudaStreamWaitEvent(st, merge.ev_join, 0);
+  }
+  if (conc) {
+    cudaEventRecord(merge.ev_join2, merge.side2);
+    cudaStreamWaitEvent(st, merge.ev_join2, 0);
   }
   return launches;
 }

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/mb
+./tools/microbench/resolve2 > gpurun_out/mb/resolve2.txt 2>&1
+cat gpurun_out/mb/resolve2.txt
