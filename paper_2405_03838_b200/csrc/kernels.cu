@@ -316,28 +316,17 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
 // n_jobs) gets A = B = kPadMargin (infeasible) and W = 0. Grid (x: blocks of
 // kProjJobs jobs, y: role * n_stages + stage). Values are recomputed from hj
 // with the projection's own functions (bit-identical to ka / kb / w).
-// part (launch_project): 0 = every role; 1 = the A and B roles only, which do not
-// depend on the quantisation range: launched right after the projection, they run
-// concurrently with it (no PDL wait before their work; they wait for the
-// projection at their end, so their completion implies its completion); 2 = the
-// W roles only (after both).
 template <int NS>
 __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restrict__ hj,
                                                            const float* __restrict__ coef_c,
                                                            const float* __restrict__ coef_d, const SpaceParams sp,
                                                            int64_t n_jobs, const unsigned long long* __restrict__ err,
-                                                           const unsigned* __restrict__ wmm, float* __restrict__ fast,
-                                                           int part) {
+                                                           const unsigned* __restrict__ wmm, float* __restrict__ fast) {
   constexpr int ld = kStageCfg + 1;  // odd: the column writes of a warp hit distinct banks
   __shared__ CoefRow s_coef[kStageCfg];
   __shared__ float s_stage[kProjWarps][32 * ld];
   __shared__ float s_nlo, s_inv;
-  int role, stage;
-  {
-    const int r = blockIdx.y / sp.n_stages;
-    stage = blockIdx.y - r * sp.n_stages;
-    role = part == 0 ? r : (part == 1 ? (r / NS) * (NS + 1) + r % NS : r * (NS + 1) + NS);
-  }
+  const int role = blockIdx.y / sp.n_stages, stage = blockIdx.y - role * sp.n_stages;
   const int slot = role / (NS + 1), kind = role % (NS + 1);  // 0 = A, NS = W, else B
   const int ncol = min(kStageCfg, sp.n_cfg - stage * kStageCfg);  // real configs in this stage
   if (threadIdx.x < ncol) {
@@ -353,20 +342,15 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
     }
     s_coef[threadIdx.x] = r;
   }
-  // part 1: the predecessor (the projection) passed its own wait, so validate's hj
-  // and err are complete; this part reads nothing the projection writes
-  if (part != 1) pdl_wait();  // the projection's w range (wmm), hj and err
+  pdl_wait();  // the projection's w range (wmm), hj and err
   pdl_launch_dependents();
-  if (threadIdx.x == 0 && kind == NS) {
+  if (threadIdx.x == 0) {
     const float inv = quant_inv<NS>(wmm);
     s_inv = inv;
     s_nlo = -__fmul_rn(unord_float_d(wmm[2 * slot]), inv);
   }
   __syncthreads();
-  if (*err != ~0ull) {
-    if (part == 1) pdl_wait();
-    return;
-  }
+  if (*err != ~0ull) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t npad = (size_t)sp.n_jobs_pad;
   float* row = s_stage[warp] + lane * ld;
@@ -401,7 +385,6 @@ __global__ void __launch_bounds__(kProjJobs) k_gather_fast(const float* __restri
   flush_rows(s_stage[warp], ld, kStageCfg, fast + (((size_t)role * sp.n_stages + stage) * npad + n0) * kStageRS, lane);
   __syncwarp();  // the staging rows are rewritten by the next chunk
   }
-  if (part == 1) pdl_wait();  // complete only once the projection is: the W part's wait covers both
 }
 
 __global__ void k_step_init(unsigned long long* err, unsigned long long* best_key, unsigned* rescore_n,
@@ -463,41 +446,19 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   // ka / kb rows only when a consumer of this step reads them (the tiled
   // scorers read the gathered layout and w); launch_project_kakb adds them later
   const int y0 = with_kakb ? 0 : sp.n_slices;
-  const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states - y0)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages)),
-      gab(jb, (unsigned)(sp.n_slots * sp.n_slots * sp.n_stages)), gw(jb, (unsigned)(sp.n_slots * sp.n_stages));
-  // the A / B roles of the gathered layout concurrently with the projection (PDL);
-  // COSCHED_SPLIT_GATHER=0: one gather launch after it
-  static const bool split_gather = [] {
-    const char* e = getenv("COSCHED_SPLIT_GATHER");
-    return !(e && e[0] == '0') && pdl_enabled();
-  }();
+  const dim3 gp(jb, (unsigned)(sp.n_slices + sp.n_slots * sp.n_states - y0)), gg(jb, (unsigned)(sp.n_roles * sp.n_stages));
   smem_optin((const void*)k_project_all<1>, 72 * 1024);
   smem_optin((const void*)k_project_all<2>, 72 * 1024);
   smem_optin((const void*)k_project_all<3>, 72 * 1024);
   if (sp.n_slots == 1) {
     launch_pdl(k_project_all<1>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    if (split_gather) {
-      launch_pdl(k_gather_fast<1>, gab, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 1);
-      launch_pdl(k_gather_fast<1>, gw, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 2);
-    } else {
-      launch_pdl(k_gather_fast<1>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 0);
-    }
+    launch_pdl(k_gather_fast<1>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else if (sp.n_slots == 2) {
     launch_pdl(k_project_all<2>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    if (split_gather) {
-      launch_pdl(k_gather_fast<2>, gab, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 1);
-      launch_pdl(k_gather_fast<2>, gw, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 2);
-    } else {
-      launch_pdl(k_gather_fast<2>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 0);
-    }
+    launch_pdl(k_gather_fast<2>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else {
     launch_pdl(k_project_all<3>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
-    if (split_gather) {
-      launch_pdl(k_gather_fast<3>, gab, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 1);
-      launch_pdl(k_gather_fast<3>, gw, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 2);
-    } else {
-      launch_pdl(k_gather_fast<3>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast, 0);
-    }
+    launch_pdl(k_gather_fast<3>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   }
 }
 

@@ -155,7 +155,11 @@ int ncclAllReduce(const void* send, void* recv, size_t count, int dtype, int op,
     }
   }
   if (!barrier(g)) return 1;  // every rank has read every slot before any slot is rewritten
-  if (bytes && cuMemcpyHtoD((CUdeviceptr)recv, acc.data(), bytes) != CUDA_SUCCESS) return 1;
+  // on the caller's stream, then synchronised: a plain cuMemcpyHtoD from pageable
+  // memory may return before the DMA lands, and the caller's (non-blocking)
+  // stream would not wait for it
+  if (bytes && cuMemcpyHtoDAsync((CUdeviceptr)recv, acc.data(), bytes, st) != CUDA_SUCCESS) return 1;
+  if (cuStreamSynchronize(st) != CUDA_SUCCESS) return 1;
   return 0;
 }
 
@@ -171,7 +175,8 @@ int ncclAllGather(const void* send, void* recv, size_t count, int dtype, ncclCom
   for (int r = 0; r < g->n; r++)
     if (bytes) memcpy(all.data() + (size_t)r * bytes, g->slot[r].data(), bytes);
   if (!barrier(g)) return 1;
-  if (!all.empty() && cuMemcpyHtoD((CUdeviceptr)recv, all.data(), all.size()) != CUDA_SUCCESS) return 1;
+  if (!all.empty() && cuMemcpyHtoDAsync((CUdeviceptr)recv, all.data(), all.size(), st) != CUDA_SUCCESS) return 1;
+  if (cuStreamSynchronize(st) != CUDA_SUCCESS) return 1;
   return 0;
 }
 
