@@ -331,6 +331,7 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.merge_tiles = n_slots == 2 ? 2 * (int64_t)num_sms() : 0;
   w.merge = (unsigned long long*)take((size_t)w.merge_tiles * 64 * 64 * 8);
   w.merge_cnt = (unsigned*)take((size_t)std::max<int64_t>(w.merge_tiles, 1) * 4);  // finished units per split tile
+  w.sel_flags = (unsigned long long*)take(256 * 8);
   w.rescore_n = (unsigned*)take(8);
   w.bytes = off;
   if (ws) *ws = w;
@@ -1016,6 +1017,8 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   uint32_t* taken_bits = ws.taken;
   CK(cudaMemsetAsync(taken_bits, 0, (size_t)((N + 31) / 32) * 4, s));
   int64_t* np_dev = ws.counters + 1;
+  CK(cudaMemsetAsync(ws.sel_flags, 0, 256 * 8, s));  // k_select_free epochs start at 1 in this call
+  unsigned sel_epoch = 0;
   unsigned long long* nk_dev = (unsigned long long*)(ws.counters + 2);
   CK(cudaMemsetAsync(np_dev, 0, 8, s));
   CK(cudaMemsetAsync(ws.counters + 8, 0, 8, s));
@@ -1130,20 +1133,30 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     // the first windows are where the batch's picks happen and block the most)
     const int64_t kWin0 = getenv("COSCHED_GREEDY_WIN0") ? std::max<int64_t>(1024, atoll(getenv("COSCHED_GREEDY_WIN0")))
                                                        : (int64_t)1 << 14;
+    static const bool cub_select = [] {  // COSCHED_GREEDY_CUBSELECT=1: CUB's DeviceSelect (A/B timing)
+      const char* e = getenv("COSCHED_GREEDY_CUBSELECT");
+      return e && e[0] == '1';
+    }();
     int r = 0;
     int64_t win = std::min(kWin0, kWin);
     for (int64_t pos = 0; pos < m; pos += win, win = std::min(kWin, 2 * win), r++) {
       const int64_t w = std::min<int64_t>(win, m - pos);
       if (pos == 0) {
         CK(launch_greedy_scan(ns, sorted, w, nullptr, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
-      } else {
+      } else if (cub_select || select_tiles(w) > 256) {
         CK(select_free_keys(ns, ws.sort_tmp, ws.sort_tmp_bytes, sorted + pos, S, cnt_dev, w, taken_bits, fmt, s));
+        CK(launch_greedy_scan(ns, S, w, cnt_dev, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
+        h->launches++;
+      } else {  // one-launch select (greedy.cu k_select_free)
+        CK(launch_select_free(ns, sorted + pos, w, taken_bits, S, cnt_dev, ws.sel_flags, ++sel_epoch, fmt, np_dev, k, s));
         CK(launch_greedy_scan(ns, S, w, cnt_dev, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
         h->launches++;
       }
       h->launches++;
       h->greedy_rounds++;
-      if ((r & 7) == 7 || pos + win >= m) {  // a host look at the pick count every 8 windows
+      // a host look at the pick count every 16 windows (windows enqueued after the
+      // k-th pick return at once: select and scan both test the count first)
+      if ((r & 15) == 15 || pos + win >= m) {
         CK(cudaMemcpyAsync(&n_picks, np_dev, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (n_picks >= k) break;

@@ -122,6 +122,7 @@ struct Workspace {
   int* pipe_ctl = nullptr;                 // [kPipeSlots + 4] ring flags, then next / done / stop
   unsigned long long* merge = nullptr;     // [merge_tiles][64 * 64] (PairMerge)
   int64_t merge_tiles = 0;
+  unsigned long long* sel_flags = nullptr;  // [256] k_select_free published tile counts (epoch-tagged)
   unsigned* merge_cnt = nullptr;            // [merge_tiles]: stage-group units done per split tile
   unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
   unsigned* rescore_n = nullptr;           // [1]
@@ -182,6 +183,13 @@ void scan_prof_report();  // COSCHED_SCAN_PROF builds: print and reset the scan 
 cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, int64_t m, const int64_t* m_dev,
                                int64_t n_jobs, uint32_t* taken_bits, unsigned long long* picks, int64_t* n_picks,
                                int64_t k_max, const GKeyFmt& fmt, cudaStream_t st, int64_t* scanned = nullptr);
+// greedy window select in one launch (greedy.cu k_select_free): the free keys of
+// the n keys at in, in order, compacted at out, their number in *m_out; flags:
+// kSelMaxTiles words zeroed once per allocation, epoch distinct per launch
+cudaError_t launch_select_free(int n_slots, const unsigned long long* in, int64_t n, const uint32_t* taken,
+                               unsigned long long* out, int64_t* m_out, unsigned long long* flags, unsigned epoch,
+                               const GKeyFmt& fmt, const int64_t* n_picks, int64_t k_max, cudaStream_t st);
+int select_tiles(int64_t n);
 int64_t pad_jobs(int64_t n_jobs);
 // node.cu
 size_t node_workspace_bytes(int64_t n_gpus, int32_t n_caps, int32_t U, int32_t gpus_per_node);

@@ -451,6 +451,8 @@ void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, i
 // about one decode per key. The taken bitmask (n_jobs bits) is the only
 // per-job state: any queue the set scorer accepts fits shared memory.
 constexpr int kScanThreads = 512, kScanPer = 4, kScanWin = kScanThreads * kScanPer, kScanWarps = kScanThreads / 32;
+// k_select_free tiles (the greedy window select, below)
+constexpr int kSelThreads = 256, kSelPer = 16, kSelTile = kSelThreads * kSelPer, kSelMaxTiles = 256;
 
 #ifdef COSCHED_SCAN_PROF
 // instrumentation build only: [0] filter cycles, [1] resolution cycles, [2] chunks,
@@ -495,6 +497,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     k_greedy_scan(const unsigned long long* __restrict__ sorted, int64_t m_host, const int64_t* __restrict__ m_dev,
                   int64_t n_jobs, uint32_t* taken_g, unsigned long long* picks, int64_t* n_picks, int64_t k_max,
                   const GKeyFmt fmt, int64_t* scanned) {
+  pdl_wait();  // the previous scan's picks and taken bits, the select's output
+  pdl_launch_dependents();
   int64_t np = *n_picks;  // warp 0's running count (uniform in warp 0)
   if (np >= k_max) return;  // uniform: enqueued windows after the k-th pick cost one launch
   const int64_t m = m_dev ? *m_dev : m_host;
@@ -605,10 +609,19 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         unsigned long long jr[kLs];
         unsigned live = 0u;
 #pragma unroll
-        for (int u = 0; u < kLs; u++) {
+        for (int u = 0; u < kLs; u++) {  // branch-free: every load of the batch in flight at once
           const int e = b0 + lane + 32 * u;
-          jr[u] = e < off ? s_sj[e] : 0ull;
-          if (e < off && jobs_packed_free<NS>(jr[u], s_taken)) live |= 1u << u;  // taken by earlier batches?
+          jr[u] = s_sj[e < off ? e : 0];
+        }
+#pragma unroll
+        for (int u = 0; u < kLs; u++) {  // taken by an earlier batch of this chunk?
+          bool fr = b0 + lane + 32 * u < off;
+#pragma unroll
+          for (int q = 0; q < NS; q++) {
+            const unsigned j = (unsigned)((jr[u] >> (20 * q)) & 0xFFFFFu);
+            fr = fr & !((s_taken[j >> 5] >> (j & 31)) & 1u);
+          }
+          live |= fr ? (1u << u) : 0u;
         }
         const long long npb = np;
 #ifdef COSCHED_SCAN_PROF
@@ -993,6 +1006,113 @@ cudaError_t launch_greedy_pipe(int n_slots, const unsigned long long* sorted, in
 size_t greedy_pipe_ring_bytes() { return sizeof(unsigned long long) * kPipeWin * kPipeLag; }
 
 // predicate of the order-preserving re-filter between scan chunks
+// The window select of the greedy scan in one launch: block q keeps, in order,
+// the keys of tile q (kSelTile consecutive keys of the sorted batch) whose jobs
+// are all free and writes them at its offset in one compacted list. The offset
+// is the sum of the earlier tiles' counts, which every block publishes as soon
+// as it has counted (tagged with the launch's epoch, so the flags need no reset
+// within an allocation); blocks start in index order, so a block only waits for
+// counts that are being computed. The last block writes the list length.
+template <int NS>
+__global__ void __launch_bounds__(kSelThreads) k_select_free(const unsigned long long* __restrict__ in, int64_t n,
+                                                             const uint32_t* __restrict__ taken,
+                                                             unsigned long long* __restrict__ out, int64_t* m_out,
+                                                             unsigned long long* flags, unsigned epoch,
+                                                             const GKeyFmt fmt, const int64_t* n_picks,
+                                                             int64_t k_max) {
+  __shared__ int s_c[kSelPer][kSelThreads / 32];
+  __shared__ long long s_off;
+  pdl_wait();  // the previous scan's taken bits
+  pdl_launch_dependents();
+  if (*n_picks >= k_max) {  // windows enqueued after the k-th pick: nothing to select
+    if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = 0;
+    return;
+  }
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int q = blockIdx.x;
+  const int64_t base = (int64_t)q * kSelTile;
+  unsigned long long k[kSelPer];
+  unsigned bm[kSelPer];
+#pragma unroll
+  for (int u = 0; u < kSelPer; u++) {
+    const int64_t i = base + u * kSelThreads + t;
+    k[u] = i < n ? __ldcs(in + i) : 0ull;
+  }
+#pragma unroll
+  for (int u = 0; u < kSelPer; u++) {
+    int32_t jb[3];
+    const bool f = k[u] != 0ull && key_jobs_free<NS>(fmt, k[u], taken, jb);
+    bm[u] = __ballot_sync(0xFFFFFFFFu, f);
+    if (lane == 0) s_c[u][wid] = __popc(bm[u]);
+  }
+  __syncthreads();
+  if (wid == 0) {
+    // exclusive prefix over the (u, warp) counts in key order: 4 per lane
+    constexpr int kPer = kSelPer * (kSelThreads / 32) / 32;
+    int* c = &s_c[0][0];
+    int v[kPer], sum = 0;
+#pragma unroll
+    for (int r = 0; r < kPer; r++) {
+      v[r] = c[lane * kPer + r];
+      sum += v[r];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int r = 0; r < kPer; r++) {
+      c[lane * kPer + r] = run;
+      run += v[r];
+    }
+    const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (lane == 0) {  // publish this tile's count
+      const unsigned long long tag = ((unsigned long long)epoch << 32) | (unsigned)tot;
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(flags + q), "l"(tag) : "memory");
+    }
+    long long off = 0;  // the earlier tiles' counts
+    for (int q0 = 0; q0 < q; q0 += 32) {
+      long long x = 0;
+      if (q0 + lane < q) {
+        unsigned long long f;
+        do {
+          asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(f) : "l"(flags + q0 + lane) : "memory");
+        } while ((unsigned)(f >> 32) != epoch);
+        x = (long long)(f & 0xFFFFFFFFull);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+      off += x;
+    }
+    if (lane == 0) {
+      s_off = off;
+      if (q == (int)gridDim.x - 1) *m_out = off + tot;
+    }
+  }
+  __syncthreads();
+  unsigned long long* o = out + s_off;
+#pragma unroll
+  for (int u = 0; u < kSelPer; u++)
+    if ((bm[u] >> lane) & 1u) o[s_c[u][wid] + __popc(bm[u] & ((1u << lane) - 1u))] = k[u];
+}
+
+cudaError_t launch_select_free(int n_slots, const unsigned long long* in, int64_t n, const uint32_t* taken,
+                               unsigned long long* out, int64_t* m_out, unsigned long long* flags, unsigned epoch,
+                               const GKeyFmt& fmt, const int64_t* n_picks, int64_t k_max, cudaStream_t st) {
+  const int64_t tiles = (n + kSelTile - 1) / kSelTile;
+  if (tiles > kSelMaxTiles) return cudaErrorInvalidValue;
+  if (tiles <= 0) return cudaSuccess;
+  if (n_slots == 2)
+    return launch_pdl(k_select_free<2>, dim3((unsigned)tiles), dim3(kSelThreads), 0, st, in, n, taken, out, m_out,
+                      flags, epoch, fmt, n_picks, k_max);
+  return launch_pdl(k_select_free<3>, dim3((unsigned)tiles), dim3(kSelThreads), 0, st, in, n, taken, out, m_out, flags,
+                    epoch, fmt, n_picks, k_max);
+}
+int select_tiles(int64_t n) { return (int)((n + kSelTile - 1) / kSelTile); }
+
 template <int NS>
 struct AllJobsFree {
   const uint32_t* bits;
@@ -1072,11 +1192,15 @@ cudaError_t launch_greedy_scan(int n_slots, const unsigned long long* sorted, in
   if (n_slots == 2) {
     cudaError_t e = smem_optin((const void*)k_greedy_scan<2>, smem);
     if (e != cudaSuccess) return e;
-    k_greedy_scan<2><<<1, kScanThreads, smem, st>>>(sorted, m, m_dev, n_jobs, taken_bits, picks, n_picks, k_max, fmt, scanned);
+    e = launch_pdl(k_greedy_scan<2>, dim3(1), dim3(kScanThreads), smem, st, sorted, m, m_dev, n_jobs, taken_bits, picks,
+                   n_picks, k_max, fmt, scanned);
+    if (e != cudaSuccess) return e;
   } else {
     cudaError_t e = smem_optin((const void*)k_greedy_scan<3>, smem);
     if (e != cudaSuccess) return e;
-    k_greedy_scan<3><<<1, kScanThreads, smem, st>>>(sorted, m, m_dev, n_jobs, taken_bits, picks, n_picks, k_max, fmt, scanned);
+    e = launch_pdl(k_greedy_scan<3>, dim3(1), dim3(kScanThreads), smem, st, sorted, m, m_dev, n_jobs, taken_bits, picks,
+                   n_picks, k_max, fmt, scanned);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

@@ -697,7 +697,10 @@ int launch_rescore(const SpaceParams& sp, const float* w, const float* fast, int
                    cudaStream_t st) {
   if (!rb.n || count <= 0) return 0;
   // up to 8 resident blocks per SM: enough loads in flight for the scan mode
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (count + 1023) / 1024));
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (count + 1023) / 1024));
+  // pairs re-score only the listed sets (normally none): one wave of blocks, each
+  // exits at once on an empty list (a 1,184-block launch costs its block scheduling)
+  if (sp.n_slots == 2 && rb.cap > 0) grid = std::min(grid, 148u);
   if (sp.n_slots == 2)
     launch_pdl(k_rescore_sets<2>, dim3(grid), dim3(256), 0, st, sp, fast, w, first, count, obj, cfg, best_key, rb, err);
   else

@@ -16,9 +16,15 @@ s = cs.Scheduler(pb)
 Fd = torch.from_numpy(F).cuda()
 s.score_all(Fd)
 torch.cuda.synchronize()
-for rep in range(2):
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+times = []
+for rep in range(reps):
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     st, ids, cfgs, tot = s.best_allocation(k)
     torch.cuda.synchronize()
-    print(f"allocation {cfgname} k={k}: {1e3 * (time.perf_counter() - t0):.2f} ms, rounds {s.greedy_rounds}, "
-          f"found {len(ids)}", flush=True)
+    times.append(1e3 * (time.perf_counter() - t0))
+    print(f"allocation {cfgname} k={k}: {times[-1]:.2f} ms, rounds {s.greedy_rounds}, found {len(ids)}", flush=True)
+if reps > 2:
+    import statistics
+    print(f"allocation {cfgname} k={k}: median of the last {reps - 1}: {statistics.median(times[1:]):.2f} ms", flush=True)
