@@ -344,6 +344,14 @@ cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* s
  * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */
 cosched_status cosched_last_timings(cosched_t h, float* ms3);
 
+/* Device time of the last step, in ms: from the event cosched_score_all records
+ * on its stream before its first kernel to the one cosched_best_set(_begin)
+ * records after the best-set detail kernel (the step's last device work; its
+ * result is then in pinned host memory). Host-side call latency before the
+ * first launch is not included. Synchronises that event. COSCHED_E_STATE unless
+ * cosched_score_all was followed by a completed cosched_best_set. */
+cosched_status cosched_last_step_ms(cosched_t h, float* ms);
+
 /* Sets of the last cosched_score_all that the tiled scorer flagged for exact
  * re-scoring (instrumentation): those whose packed-objective choice was not
  * provably within tau/2 = 5e-6 relative of the exact FP32 argmax (objective

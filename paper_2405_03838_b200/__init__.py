@@ -226,6 +226,12 @@ class Scheduler:
         (record an event after it to time the step's device work), then call best_set_end."""
         self._check(self._L.cosched_best_set_begin(self._h))
 
+    def last_step_ms(self) -> float:
+        """Device time of the last score_all + best_set (library events around the step's kernels)."""
+        ms = ctypes.c_float()
+        self._check(self._L.cosched_last_step_ms(self._h, ctypes.byref(ms)))
+        return ms.value
+
     def best_set_end(self):
         """Synchronise and return best_set's (status, set_id, cfg, obj)."""
         sid, cfg, obj = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_float()

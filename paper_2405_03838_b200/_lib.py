@@ -89,6 +89,7 @@ SIGNATURES = [
     ("cosched_local_best_key", I32, [P, P]),
     ("cosched_best_set", I32, [P, P, P, P]),
     ("cosched_best_set_begin", I32, [P]),
+    ("cosched_last_step_ms", I32, [P, P]),
     ("cosched_best_set_end", I32, [P, P, P, P]),
     ("cosched_best_config", I32, [P, I64, P, P, P, P, P]),
     ("cosched_best_allocation", I32, [P, I32, P, P, P, P]),

@@ -130,6 +130,7 @@ struct cosched_ctx {
   int view_nranks = 1;  // shard view without comm (tests)
   int64_t greedy_rounds = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t evp[3] = {nullptr, nullptr, nullptr};  // COSCHED_PREP_EVENTS: after step init, validate, projection
   cudaStream_t side = nullptr;                 // partial-column units of the pair scorer (PairMerge)
   cudaStream_t side2 = nullptr;                // its stage-split tail units
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
@@ -525,6 +526,8 @@ void cosched_destroy(cosched_t h) {
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
     for (int i = 0; i < 4; i++)
       if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+    for (auto& e : h->evp)
+      if (e) cudaEventDestroy(e);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ev_join2) cudaEventDestroy(h->ev_join2);
@@ -747,6 +750,15 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   cudaEventRecord(h->ev[0], st);
   launch_step_init(ws.err, ws.best_key, ws.rescore_n, ws.wmm, st);
   h->launches += 1;
+  // instrumentation (COSCHED_PREP_EVENTS=1): the prep's parts, printed by
+  // cosched_last_timings; the extra events cut the PDL overlap they measure across
+  static const bool prep_events = [] {
+    const char* e = getenv("COSCHED_PREP_EVENTS");
+    return e && e[0] == '1';
+  }();
+  if (prep_events && !h->evp[0])
+    for (auto& e : h->evp) cudaEventCreate(&e);
+  if (prep_events) cudaEventRecord(h->evp[0], st);
   {
     // rows of the gathered layout the tiled scorer reads for this shard: the
     // sets' largest positions lie in [c0, c1), every other position below c1
@@ -776,12 +788,14 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   }
   if (n_jobs > 0) {
     launch_validate(features_dev, n_rows, jobs_dev, n_jobs, ws.err, ws.hj, st);
+    if (prep_events) cudaEventRecord(h->evp[1], st);
     // the tiled scorers read only the gathered layout and w: ka / kb are
     // projected later, and only if a consumer (detail of arbitrary sets, node
     // budget, exact allocation) asks for them
     const bool tiled = h->variant != 0 && h->sp.search_mode == 0 && tiled_applicable(h->n_slots, n_jobs, first, count);
     h->kakb_valid = !tiled;
-    launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, !tiled, st);
+    launch_project(ws.hj, n_jobs, h->sp, h->tb, ws.err, ws.ka, ws.kb, ws.w, ws.fast, ws.wmm, !tiled, st,
+                   prep_events ? h->evp[2] : nullptr);
     h->launches += 3;
   }
   cudaEventRecord(h->ev[1], st);
@@ -850,6 +864,23 @@ cosched_status cosched_last_timings(cosched_t h, float* ms3) {
   CK(cudaEventElapsedTime(&ms3[0], h->ev[0], h->ev[1]));
   CK(cudaEventElapsedTime(&ms3[1], h->ev[1], h->ev[2]));
   CK(cudaEventElapsedTime(&ms3[2], h->ev[0], h->ev[2]));
+  if (h->evp[0] && getenv("COSCHED_PREP_EVENTS")) {
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, h->ev[0], h->evp[0]);
+    cudaEventElapsedTime(&b, h->evp[0], h->evp[1]);
+    cudaEventElapsedTime(&c, h->evp[1], h->evp[2]);
+    cudaEventElapsedTime(&d, h->evp[2], h->ev[1]);
+    fprintf(stderr, "prep: init %.4f validate %.4f project %.4f gather %.4f ms\n", a, b, c, d);
+  }
+  return COSCHED_OK;
+}
+
+cosched_status cosched_last_step_ms(cosched_t h, float* ms) {
+  if (!h || !ms) return fail(h, COSCHED_E_ARG, "null argument");
+  if (!h->scored || h->best_pending) return fail(h, COSCHED_E_STATE, "needs cosched_score_all then cosched_best_set");
+  DeviceGuard g(h->device);
+  CK(cudaEventSynchronize(h->ev[3]));
+  CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[3]));
   return COSCHED_OK;
 }
 
@@ -903,6 +934,7 @@ cosched_status cosched_best_set_begin(cosched_t h) {
   launch_best_detail(h->sp, h->ws.ka, h->ws.kb, h->ws.w, h->ws.best_key, h->ws.err, h->h_pinned, h->ws.hj,
                      h->kakb_valid ? nullptr : &h->tb, h->stream);
   h->launches++;
+  cudaEventRecord(h->ev[3], h->stream);  // end of the step's device work (cosched_last_step_ms)
   h->best_pending = true;
   return COSCHED_OK;
 }

@@ -213,7 +213,7 @@ void launch_validate(const float* features, int64_t n_rows, const int32_t* jobs,
                      unsigned long long* err, float* hj, cudaStream_t st);
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
-                    bool with_kakb, cudaStream_t st);
+                    bool with_kakb, cudaStream_t st, cudaEvent_t mid = nullptr);
 // the ka / kb rows alone, after a launch_project without them
 void launch_project_kakb(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                          const unsigned long long* err, float* ka, float* kb, unsigned* wmm_scratch, cudaStream_t st);

@@ -434,7 +434,7 @@ void launch_step_init(unsigned long long* err, unsigned long long* best_key, uns
 
 void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
                     const unsigned long long* err, float* ka, float* kb, float* w, float* fast, unsigned* wmm,
-                    bool with_kakb, cudaStream_t st) {
+                    bool with_kakb, cudaStream_t st, cudaEvent_t mid) {
   if (n_jobs <= 0) return;  // wmm was reset by launch_step_init
   // 2 job chunks of 128 per block (measured on C4: 1 -> 60.4 us, 2 -> 58.9,
   // 4 -> 62.1, 8 -> 75.2 for project + gather; COSCHED_PROJ_CHUNKS overrides)
@@ -452,12 +452,15 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   smem_optin((const void*)k_project_all<3>, 72 * 1024);
   if (sp.n_slots == 1) {
     launch_pdl(k_project_all<1>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<1>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else if (sp.n_slots == 2) {
     launch_pdl(k_project_all<2>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<2>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else {
     launch_pdl(k_project_all<3>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<3>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   }
 }
