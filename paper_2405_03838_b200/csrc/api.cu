@@ -116,8 +116,8 @@ struct cosched_ctx {
   unsigned long long* h_pinned = nullptr;  // [8] pinned host readback
   // last score_all
   bool scored = false;
-  bool kakb_valid = false;
-  bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called  // ka / kb rows of this step's projection present (else launch_project_kakb on demand)
+  bool kakb_valid = false;    // ka / kb rows (and every w row) of this step's projection present (else ensure_kakb)
+  bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
   Workspace ws{};
@@ -900,7 +900,9 @@ cosched_status cosched_local_best_key(cosched_t h, uint64_t* key) {
 static void ensure_kakb(cosched_t h) {
   if (h->kakb_valid) return;
   if (h->n_jobs > 0) {
-    launch_project_kakb(h->ws.hj, h->n_jobs, h->sp, h->tb, h->ws.err, h->ws.ka, h->ws.kb, h->ws.wmm, h->stream);
+    // the tiled step stored only the w rows its own scorer reads: complete them too
+    launch_project_kakb(h->ws.hj, h->n_jobs, h->sp, h->tb, h->ws.err, h->ws.ka, h->ws.kb, h->ws.wmm, h->stream,
+                        h->ws.w);
     h->launches++;
   }
   h->kakb_valid = true;

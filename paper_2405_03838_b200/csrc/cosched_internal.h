@@ -216,7 +216,8 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
                     bool with_kakb, cudaStream_t st, cudaEvent_t mid = nullptr);
 // the ka / kb rows alone, after a launch_project without them
 void launch_project_kakb(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
-                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm_scratch, cudaStream_t st);
+                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm, cudaStream_t st,
+                         float* w_full = nullptr);
 // Hill climbing for sets [first, first+count) (search_mode 1); adds the f evaluations to *evals.
 int launch_score_hill(const SpaceParams& sp, int64_t n_jobs, const float* ka, const float* kb, const float* w,
                       int64_t first, int64_t count, float* obj, int32_t* cfg, unsigned long long* best_key,

@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
                                                            const float* __restrict__ coef_d,
                                                            const unsigned long long* __restrict__ err,
                                                            float* __restrict__ ka, float* __restrict__ kb,
-                                                           float* __restrict__ w, unsigned* wmm, int y0) {
+                                                           float* __restrict__ w, unsigned* wmm, int y0,
+                                                           int w_partial) {
   __shared__ CoefRow s_coef[kMaxCaps];
   __shared__ unsigned s_mm[2];
   extern __shared__ float s_stage[];  // [2][kProjWarps][32][rs + 1]
@@ -276,7 +277,10 @@ __global__ void __launch_bounds__(kProjJobs) k_project_all(const float* __restri
       }
       for (int p = nc; p < rs; p++) row_a[p] = -1e30f;
       __syncwarp();
-      flush_rows(stg_a, ld, rs, w + ((((size_t)slot * sp.n_states + state) * npad) + n0) * rs, lane);
+      // w_partial (a tiled step): only the rows this rank's scorer reads are stored
+      // (the range above still covers every job); ensure_kakb completes the rest
+      if (!w_partial || (n0 + 32 > sp.fast_lo[slot] && n0 < sp.fast_hi[slot]))
+        flush_rows(stg_a, ld, rs, w + ((((size_t)slot * sp.n_states + state) * npad) + n0) * rs, lane);
     }
     __syncwarp();  // the staging rows are rewritten by the next chunk
   }
@@ -451,15 +455,18 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
   smem_optin((const void*)k_project_all<2>, 72 * 1024);
   smem_optin((const void*)k_project_all<3>, 72 * 1024);
   if (sp.n_slots == 1) {
-    launch_pdl(k_project_all<1>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_project_all<1>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0,
+               with_kakb ? 0 : 1);
     if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<1>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else if (sp.n_slots == 2) {
-    launch_pdl(k_project_all<2>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_project_all<2>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0,
+               with_kakb ? 0 : 1);
     if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<2>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   } else {
-    launch_pdl(k_project_all<3>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0);
+    launch_pdl(k_project_all<3>, gp, dim3(kProjJobs), stage_bytes, st, hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w, wmm, y0,
+               with_kakb ? 0 : 1);
     if (mid) cudaEventRecord(mid, st);
     launch_pdl(k_gather_fast<3>, gg, dim3(kProjJobs), 0, st, hj, tb.coef_c, tb.coef_d, sp, n_jobs, err, wmm, fast);
   }
@@ -467,22 +474,24 @@ void launch_project(const float* hj, int64_t n_jobs, const SpaceParams& sp, cons
 
 // The ka / kb rows alone (after a launch_project without them).
 void launch_project_kakb(const float* hj, int64_t n_jobs, const SpaceParams& sp, const DeviceTables& tb,
-                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm_scratch, cudaStream_t st) {
+                         const unsigned long long* err, float* ka, float* kb, unsigned* wmm, cudaStream_t st,
+                         float* w_full) {
   if (n_jobs <= 0) return;
   const int64_t n_chunks = (sp.n_jobs_pad + kProjJobs - 1) / kProjJobs;
   const unsigned jb = (unsigned)((n_chunks + 1) / 2);
   const size_t stage_bytes = (size_t)2 * kProjWarps * 32 * (sp.rs + 1) * sizeof(float);
-  const dim3 gp(jb, (unsigned)sp.n_slices);
-  // the grid covers rows y < n_slices only: the w rows (and wmm) are untouched
+  // rows y < n_slices (ka / kb); with w_full also every w row, recomputed bit-identically
+  // (the w range it folds into wmm is the one the step already reduced: unchanged)
+  const dim3 gp(jb, (unsigned)(sp.n_slices + (w_full ? sp.n_slots * sp.n_states : 0)));
   if (sp.n_slots == 1)
-    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
-                                                         wmm_scratch, 0);
+    k_project_all<1><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w_full, wmm,
+                                                         0, 0);
   else if (sp.n_slots == 2)
-    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
-                                                         wmm_scratch, 0);
+    k_project_all<2><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w_full, wmm,
+                                                         0, 0);
   else
-    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, nullptr,
-                                                         wmm_scratch, 0);
+    k_project_all<3><<<gp, kProjJobs, stage_bytes, st>>>(hj, n_jobs, sp, tb.coef_c, tb.coef_d, err, ka, kb, w_full, wmm,
+                                                         0, 0);
 }
 
 // ---------------------------------------------------------------------------
