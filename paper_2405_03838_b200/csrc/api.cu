@@ -118,6 +118,7 @@ struct cosched_ctx {
   bool scored = false;
   bool kakb_valid = false;    // ka / kb rows (and every w row) of this step's projection present (else ensure_kakb)
   bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called
+  bool step_timed = false;    // ev[3] recorded after this score_all's best-set detail kernel
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
   Workspace ws{};
@@ -332,7 +333,7 @@ size_t workspace_layout(int64_t n_jobs, const SpaceParams& sp, int64_t n_sets_lo
   w.merge_tiles = n_slots == 2 ? 2 * (int64_t)num_sms() : 0;
   w.merge = (unsigned long long*)take((size_t)w.merge_tiles * 64 * 64 * 8);
   w.merge_cnt = (unsigned*)take((size_t)std::max<int64_t>(w.merge_tiles, 1) * 4);  // finished units per split tile
-  w.sel_flags = (unsigned long long*)take(256 * 8);
+  w.sel_flags = (unsigned long long*)take(1024 * 8);  // k_select_free tiles: windows up to 4 M keys
   w.rescore_n = (unsigned*)take(8);
   w.bytes = off;
   if (ws) *ws = w;
@@ -825,6 +826,7 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
   h->scored = true;
+  h->step_timed = false;
   h->n_jobs = n_jobs;
   h->first = first;
   h->n_sets = count;
@@ -877,7 +879,8 @@ cosched_status cosched_last_timings(cosched_t h, float* ms3) {
 
 cosched_status cosched_last_step_ms(cosched_t h, float* ms) {
   if (!h || !ms) return fail(h, COSCHED_E_ARG, "null argument");
-  if (!h->scored || h->best_pending) return fail(h, COSCHED_E_STATE, "needs cosched_score_all then cosched_best_set");
+  if (!h->scored || h->best_pending || !h->step_timed)
+    return fail(h, COSCHED_E_STATE, "needs cosched_score_all then cosched_best_set");
   DeviceGuard g(h->device);
   CK(cudaEventSynchronize(h->ev[3]));
   CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[3]));
@@ -938,6 +941,7 @@ cosched_status cosched_best_set_begin(cosched_t h) {
   h->launches++;
   cudaEventRecord(h->ev[3], h->stream);  // end of the step's device work (cosched_last_step_ms)
   h->best_pending = true;
+  h->step_timed = true;
   return COSCHED_OK;
 }
 
@@ -1051,7 +1055,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
   uint32_t* taken_bits = ws.taken;
   CK(cudaMemsetAsync(taken_bits, 0, (size_t)((N + 31) / 32) * 4, s));
   int64_t* np_dev = ws.counters + 1;
-  CK(cudaMemsetAsync(ws.sel_flags, 0, 256 * 8, s));  // k_select_free epochs start at 1 in this call
+  CK(cudaMemsetAsync(ws.sel_flags, 0, 1024 * 8, s));  // k_select_free epochs start at 1 in this call
   unsigned sel_epoch = 0;
   unsigned long long* nk_dev = (unsigned long long*)(ws.counters + 2);
   CK(cudaMemsetAsync(np_dev, 0, 8, s));
@@ -1161,8 +1165,13 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
     // start reach the one-block scan.
     unsigned long long* S = h->comm ? ws.gath : (unsigned long long*)ws.alive;
     int64_t* cnt_dev = ws.counters + 3;
+    // largest window: 256 K keys when picks are dense in the key order (C4: 5,000
+    // picks in 5x10^7 sets), 1 M when sparse (C5: 666 in 1.3x10^9) -- fewer
+    // select + scan launches for the same survivors (tools/alloc_prof.py: C4
+    // 6.9 / 7.4 / 9.1 ms and C5 37.7 / 31.3 / 31.3 ms at 256 K / 1 M / 4 M)
+    const double pick_density = (double)k / (double)std::max<int64_t>(cosched::n_sets(N, ns), 1);
     const int64_t kWin = getenv("COSCHED_GREEDY_CHUNK") ? std::max<int64_t>(1024, atoll(getenv("COSCHED_GREEDY_CHUNK")))
-                                                       : (int64_t)1 << 18;
+                                                       : (pick_density < 1e-5 ? (int64_t)1 << 20 : (int64_t)1 << 18);
     // windows grow from kWin0 (the batch's first keys are all free at its start:
     // the first windows are where the batch's picks happen and block the most)
     const int64_t kWin0 = getenv("COSCHED_GREEDY_WIN0") ? std::max<int64_t>(1024, atoll(getenv("COSCHED_GREEDY_WIN0")))
@@ -1177,7 +1186,7 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       const int64_t w = std::min<int64_t>(win, m - pos);
       if (pos == 0) {
         CK(launch_greedy_scan(ns, sorted, w, nullptr, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
-      } else if (cub_select || select_tiles(w) > 256) {
+      } else if (cub_select || select_tiles(w) > 1024) {
         CK(select_free_keys(ns, ws.sort_tmp, ws.sort_tmp_bytes, sorted + pos, S, cnt_dev, w, taken_bits, fmt, s));
         CK(launch_greedy_scan(ns, S, w, cnt_dev, N, taken_bits, ws.picked, np_dev, k, fmt, s, ws.counters + 8));
         h->launches++;

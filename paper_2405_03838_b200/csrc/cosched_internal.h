@@ -122,7 +122,7 @@ struct Workspace {
   int* pipe_ctl = nullptr;                 // [kPipeSlots + 4] ring flags, then next / done / stop
   unsigned long long* merge = nullptr;     // [merge_tiles][64 * 64] (PairMerge)
   int64_t merge_tiles = 0;
-  unsigned long long* sel_flags = nullptr;  // [256] k_select_free published tile counts (epoch-tagged)
+  unsigned long long* sel_flags = nullptr;  // [1024] k_select_free published tile counts (epoch-tagged)
   unsigned* merge_cnt = nullptr;            // [merge_tiles]: stage-group units done per split tile
   unsigned* rescore_list = nullptr;        // [rescore_cap] (RescoreBuf)
   unsigned* rescore_n = nullptr;           // [1]

@@ -318,23 +318,55 @@ __global__ void __launch_bounds__(32 * kKirWarps) k_keys_live(const int32_t* __r
       s0 = c3(j[2]) + c2(j[1]);
     }
     const int64_t lo_i = s0 > first ? s0 : first, hi_i = s0 + j[1] < first + count ? s0 + j[1] : first + count;
-    for (int64_t base = lo_i; base < hi_i; base += 32) {  // warp-uniform
-      const int64_t sid = base + lane;
-      bool ok = false;
-      unsigned long long kk = 0ull;
-      if (sid < hi_i) {
-        const float o = __ldcs(obj + (sid - first));
-        j[0] = sid - s0;
-        if (__float_as_uint(o) - b_lo < r_w && !((__ldg(taken_bits + (j[0] >> 5)) >> (j[0] & 31)) & 1u)) {
-          ok = true;
-          kk = gkey_make<NS>(fmt, o, sid, j);
+    if (lo_i >= hi_i) continue;
+    // the row's objectives [lo_i, hi_i) as aligned float4s of the shard's array
+    // (a lane takes 4 consecutive elements, elements outside the row are
+    // masked), two 512-byte warp loads in flight per step; key order within a
+    // batch list does not matter (it is sorted next)
+    const int64_t e_lo = lo_i - first, e_hi = hi_i - first;  // element range in obj
+    const int64_t mis = (int64_t)((reinterpret_cast<uintptr_t>(obj) >> 2) & 3);
+    int64_t b4 = ((e_lo + mis) & ~3ll) - mis;  // first element of the first 16-byte group
+    for (; b4 < e_hi; b4 += 2 * 128) {  // warp-uniform
+      float v[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t e0 = b4 + h * 128 + 4 * lane;
+        if (b4 + h * 128 >= e_hi) {  // warp-uniform: past the row
+#pragma unroll
+          for (int q = 0; q < 4; q++) v[h][q] = -INFINITY;
+        } else if (e0 >= 0 && e0 + 3 < count) {
+          const float4 f = __ldcs(reinterpret_cast<const float4*>(obj + e0));
+          v[h][0] = f.x;
+          v[h][1] = f.y;
+          v[h][2] = f.z;
+          v[h][3] = f.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) v[h][q] = (e0 + q >= 0 && e0 + q < count) ? obj[e0 + q] : -INFINITY;
         }
       }
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
-      if (ok) ob[on + __popc(m & ((1u << lane) - 1u))] = kk;
-      on += __popc(m);
-      __syncwarp();
-      if (on > kKirOut - 32) flush();
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int64_t e = b4 + h * 128 + 4 * lane + q;
+          bool ok = false;
+          unsigned long long kk = 0ull;
+          if (e >= e_lo && e < e_hi && __float_as_uint(v[h][q]) - b_lo < r_w) {
+            j[0] = e + first - s0;
+            if (!((__ldg(taken_bits + (j[0] >> 5)) >> (j[0] & 31)) & 1u)) {
+              ok = true;
+              kk = gkey_make<NS>(fmt, v[h][q], e + first, j);
+            }
+          }
+          const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+          if (m) {
+            if (ok) ob[on + __popc(m & ((1u << lane) - 1u))] = kk;
+            on += __popc(m);
+            __syncwarp();
+            if (on > kKirOut - 32) flush();
+          }
+        }
     }
   }
   flush();
@@ -452,7 +484,7 @@ void launch_free_sets(int n_slots, const uint32_t* taken_bits, int64_t n_jobs, i
 // per-job state: any queue the set scorer accepts fits shared memory.
 constexpr int kScanThreads = 512, kScanPer = 4, kScanWin = kScanThreads * kScanPer, kScanWarps = kScanThreads / 32;
 // k_select_free tiles (the greedy window select, below)
-constexpr int kSelThreads = 256, kSelPer = 16, kSelTile = kSelThreads * kSelPer, kSelMaxTiles = 256;
+constexpr int kSelThreads = 256, kSelPer = 16, kSelTile = kSelThreads * kSelPer, kSelMaxTiles = 1024;
 
 #ifdef COSCHED_SCAN_PROF
 // instrumentation build only: [0] filter cycles, [1] resolution cycles, [2] chunks,
