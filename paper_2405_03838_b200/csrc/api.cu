@@ -1136,6 +1136,9 @@ static cosched_status greedy_sorted_scan(cosched_t h, int32_t k, std::vector<uns
       m = mx * W;
     }
     CK(sort_keys_desc(ws.sort_tmp, ws.sort_tmp_bytes, list, sorted, m, s, fmt.end_bit));
+    if (getenv("COSCHED_GREEDY_STATS"))
+      fprintf(stderr, "greedy batch: bins [%d, %d], %lld keys sorted on %d bits%s\n", bin_lo, bin_hi, (long long)m,
+              fmt.end_bit, endgame ? " (endgame)" : "");
     h->launches++;
     if (getenv("COSCHED_GREEDY_PIPE") && atoi(getenv("COSCHED_GREEDY_PIPE")) != 0) {
       // (COSCHED_GREEDY_PIPE=1, measured slower on C4: DESIGN.md §5) the whole sorted
