@@ -298,74 +298,66 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
     if (!SPLIT && s == sp.n_stages - 1) {
-      // ---- tile end: park each pair's best key, then resolve and write with a
-      // rolled loop in which a warp owns 32 consecutive j0 of one column
-      // (128-byte coalesced obj/cfg writes)
+      // ---- tile end, owner first: each thread resolves its own 4 x 4 pairs with
+      // all 32 w loads in flight, parks (objective, config) in shared memory; a
+      // rolled loop then writes them with 128-byte coalesced stores (r01's
+      // resolve-in-the-store-loop, 4 pairs' loads per pass: 3.030 -> 3.022 ms on C4).
+      // A positive fairness margin is >= 8 (kScale, cosched_internal.h) and a
+      // packed key is < 4.0, so the best masked key of a feasible pair is never
+      // clipped: its low bits are the stage offset of the argmax, and the
+      // reported objective is the exact FP32 w0 + w1 of that config (2 loads).
+      const int jI = (int)(I * kTile), jJ = (int)(J * kTile);
+      const int c_lo = (int)g.c0, c_hi = (int)g.c1;
+      const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
+      int cc[kM][NB];
+      float f0[kM][NB], f1[kM][NB];
 #pragma unroll
       for (int a = 0; a < kM; a++)
 #pragma unroll
         for (int b = 0; b < NB; b++) {
-          sbest[(ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a] = breg[a][b];
+          const int e = (ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a;
+          const int j0 = jI + tx + 16 * a, j1 = jJ + ty + 16 * (b0 + b);
+          const int sg = sbg[e];  // this thread's own entry
+          const unsigned kbits = __float_as_uint(breg[a][b]);
           breg[a][b] = 0.0f;
-        }
-      __syncthreads();
-      // 4 pairs per pass with all their loads in flight (no register spills;
-      // 2: 3.22 ms, 8: 3.20 ms, 4: 3.17 ms on C4). A positive fairness
-      // margin is >= 8 (kScale, cosched_internal.h) and a packed key is < 4.0, so
-      // the best masked key of a feasible pair is never clipped: its low bits
-      // are the stage offset of the argmax, and the reported objective is the
-      // exact FP32 w0 + w1 of that config (2 loads).
-      constexpr int kPass = 4;
-      const int jI = (int)(I * kTile), jJ = (int)(J * kTile);
-      const int c_lo = (int)g.c0, c_hi = (int)g.c1;  // this shard's columns (c1 <= n_jobs)
-      const int rsz = sp.rs, npad = (int)sp.n_jobs_pad, w1base = sp.n_states * npad;
-      const float thr = s_thr;
-#pragma unroll 1
-      for (int e0 = 16 * kTile * b0; e0 < 16 * kTile * (b0 + NB); e0 += kPass * kThreads) {
-        float f0[kPass], f1[kPass];
-        int c_[kPass];
-#pragma unroll
-        for (int u = 0; u < kPass; u++) {
-          const int e = e0 + u * kThreads + threadIdx.x;
-          const int rj = e >> 6, ri = e & 63;
-          const int j0 = jI + ri, j1 = jJ + rj;
-          const int sg = sbg[rj * kBgRow + ri];  // read and reset every slot, valid or not
-          const unsigned kbits = __float_as_uint(sbest[rj * kBgRow + ri]);
-          sbg[rj * kBgRow + ri] = -1;
           const bool ok = j0 < j1 && j1 >= c_lo && j1 < c_hi;
           const int c = sg * kStageCfg + 31 - (int)(kbits & 31u);
-          c_[u] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
-          f0[u] = f1[u] = 0.0f;
-          if (c_[u] >= 0) {
-            // c / n_caps in FP32: (c + 0.5) / n_caps stays >= 1/128 away from an
-            // integer for c < 2^13, n_caps <= 64, so the truncation is exact
+          cc[a][b] = (ok && sg >= 0 && c < sp.n_cfg) ? c : (ok ? -1 : -2);
+          f0[a][b] = f1[a][b] = 0.0f;
+          if (cc[a][b] >= 0) {
             const int st = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st * sp.n_caps;
-            const int r0 = st * npad + j0, r1 = w1base + st * npad + j1;  // w rows, < 2^31
-            f0[u] = __ldg(w + (int64_t)r0 * rsz + p);
-            f1[u] = __ldg(w + (int64_t)r1 * rsz + p);
+            f0[a][b] = __ldg(w + (int64_t)(st * npad + j0) * rsz + p);
+            f1[a][b] = __ldg(w + (int64_t)(w1base + st * npad + j1) * rsz + p);
           }
         }
 #pragma unroll
-        for (int u = 0; u < kPass; u++) {
-          if (c_[u] == -2) continue;
-          const int e = e0 + u * kThreads + threadIdx.x;
-          const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0 of one column
-          const int j0 = jI + ri, j1 = jJ + rj;
-          const int bc = c_[u];
-          const float bo = bc >= 0 ? __fadd_rn(f0[u], f1[u]) : -INFINITY;
-          const int64_t sid = (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
-          const int64_t k = sid - g.first_set;
-          if (out_obj) out_obj[k] = bo;
-          if (out_cfg) out_cfg[k] = bc;
-          if (bc >= 0) {
-            const unsigned long long kk = pack_key(bo, sid);
-            key = kk > key ? kk : key;
-#ifndef COSCHED_VAR_NOFLAG
-            if (bo < thr) {  // not provably within tau/2 of the FP32 argmax: exact re-score
-              const unsigned at = atomicAdd(rb.n, 1u);
-              if (at < rb.cap) rb.list[at] = (unsigned)k;
-            }
-#endif
+      for (int a = 0; a < kM; a++)
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+          const int e = (ty + 16 * (b0 + b)) * kBgRow + tx + 16 * a;
+          sbest[e] = cc[a][b] >= 0 ? __fadd_rn(f0[a][b], f1[a][b]) : -INFINITY;
+          sbg[e] = (int16_t)cc[a][b];
+        }
+      __syncthreads();
+      const float thr = s_thr;
+#pragma unroll 4
+      for (int e = 16 * kTile * b0 + threadIdx.x; e < 16 * kTile * (b0 + NB); e += kThreads) {
+        const int rj = e >> 6, ri = e & 63;  // a warp writes 32 consecutive j0 of one column
+        const int bc = sbg[rj * kBgRow + ri];
+        const float bo = sbest[rj * kBgRow + ri];
+        sbg[rj * kBgRow + ri] = -1;
+        if (bc == -2) continue;
+        const int j0 = jI + ri, j1 = jJ + rj;
+        const int64_t sid = (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
+        const int64_t k = sid - g.first_set;
+        if (out_obj) out_obj[k] = bo;
+        if (out_cfg) out_cfg[k] = bc;
+        if (bc >= 0) {
+          const unsigned long long kk = pack_key(bo, sid);
+          key = kk > key ? kk : key;
+          if (bo < thr) {  // not provably within tau/2 of the FP32 argmax: exact re-score
+            const unsigned at = atomicAdd(rb.n, 1u);
+            if (at < rb.cap) rb.list[at] = (unsigned)k;
           }
         }
       }
