@@ -799,7 +799,13 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
                    prep_events ? h->evp[2] : nullptr);
     h->launches += 3;
   }
-  cudaEventRecord(h->ev[1], st);
+  // prep / score split for cosched_last_timings (COSCHED_NO_EV1=1: not recorded,
+  // A/B of whether an event between the gather and the scorer costs the PDL overlap)
+  static const bool no_ev1 = [] {
+    const char* e = getenv("COSCHED_NO_EV1");
+    return e && e[0] == '1';
+  }();
+  if (!no_ev1) cudaEventRecord(h->ev[1], st);
   if (h->sp.search_mode == 1) {
     launch_fill_u64((unsigned long long*)(ws.counters + 7), 0ull, 1, st);
     h->launches += 1 + launch_score_hill(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key,

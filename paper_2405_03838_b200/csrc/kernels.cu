@@ -837,7 +837,7 @@ __device__ __forceinline__ void eval_any(const SpaceParams& sp, const float* __r
 // RPerf / Throughput / Fairness -- no second evaluation. HJ: operands from the
 // basis rows (staged in shared memory) and the coefficient tables.
 template <bool HJ>
-__global__ void __launch_bounds__(256) k_sets_detail(const SpaceParams sp, const float* __restrict__ ka,
+__global__ void __launch_bounds__(512) k_sets_detail(const SpaceParams sp, const float* __restrict__ ka,
                                                      const float* __restrict__ kb, const float* __restrict__ w,
                                                      const int64_t* __restrict__ set_ids,
                                                      const unsigned long long* __restrict__ key_src, float* out_all,
@@ -959,11 +959,14 @@ void launch_best_detail(const SpaceParams& sp, const float* ka, const float* kb,
   // operands from hj and the coefficient tables (no ka / kb this step)
   const int64_t* no_ids = nullptr;
   const float* no_tab = nullptr;
+  // one config per thread (one round of the evaluation's dependent loads): the
+  // best set's detail is the step's last kernel
+  const unsigned nt = (unsigned)std::min(512, std::max(32, (sp.n_cfg + 31) / 32 * 32));
   if (tb)
-    launch_pdl(k_sets_detail<true>, dim3(1), dim3(256), 0, st, sp, ka, kb, w, no_ids, key,
+    launch_pdl(k_sets_detail<true>, dim3(1), dim3(nt), 0, st, sp, ka, kb, w, no_ids, key,
                reinterpret_cast<float*>(host_out + 2), err, host_out, hj, tb->coef_c, tb->coef_d);
   else
-    launch_pdl(k_sets_detail<false>, dim3(1), dim3(256), 0, st, sp, ka, kb, w, no_ids, key,
+    launch_pdl(k_sets_detail<false>, dim3(1), dim3(nt), 0, st, sp, ka, kb, w, no_ids, key,
                reinterpret_cast<float*>(host_out + 2), err, host_out, no_tab, no_tab, no_tab);
 }
 
