@@ -339,9 +339,16 @@ cosched_status cosched_node_budget(cosched_t h, int64_t n_gpus, const int64_t* s
                                    double node_power_w, int32_t objective, void* workspace, size_t workspace_bytes,
                                    int32_t* caps_out, int32_t* cfgs_out, float* node_obj, void* cuda_stream);
 
+/* Record (on = 1) or not (0, the default) the events cosched_last_timings
+ * reads: one between the gather and the scorer and one after the scorer. They
+ * cost the scorer's launch its overlap with the gather's tail (programmatic
+ * dependent launch, ~5 us a step), so timing runs ask for them explicitly. */
+cosched_status cosched_set_timing(cosched_t h, int on);
+
 /* Device time (ms, CUDA events on the caller's stream) of the last
  * cosched_score_all: ms[0] = validate + basis + projection, ms[1] = the set
- * scorer (the dominant kernel), ms[2] = the whole call. Synchronises. */
+ * scorer (the dominant kernel), ms[2] = the whole call. Synchronises.
+ * COSCHED_E_STATE unless that call ran with cosched_set_timing(h, 1). */
 cosched_status cosched_last_timings(cosched_t h, float* ms3);
 
 /* Device time of the last step, in ms: from the event cosched_score_all records

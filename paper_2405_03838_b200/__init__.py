@@ -226,6 +226,11 @@ class Scheduler:
         (record an event after it to time the step's device work), then call best_set_end."""
         self._check(self._L.cosched_best_set_begin(self._h))
 
+    def set_timing(self, on: bool):
+        """Record the prep / score split events read by last_timings (off by default: they
+        cost the scorer's launch its overlap with the gather)."""
+        self._check(self._L.cosched_set_timing(self._h, 1 if on else 0))
+
     def last_step_ms(self) -> float:
         """Device time of the last score_all + best_set (library events around the step's kernels)."""
         ms = ctypes.c_float()

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("cosched_best_set", I32, [P, P, P, P]),
     ("cosched_best_set_begin", I32, [P]),
     ("cosched_last_step_ms", I32, [P, P]),
+    ("cosched_set_timing", I32, [P, I32]),
     ("cosched_best_set_end", I32, [P, P, P, P]),
     ("cosched_best_config", I32, [P, I64, P, P, P, P, P]),
     ("cosched_best_allocation", I32, [P, I32, P, P, P, P]),

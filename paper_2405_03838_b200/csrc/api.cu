@@ -119,6 +119,8 @@ struct cosched_ctx {
   bool kakb_valid = false;    // ka / kb rows (and every w row) of this step's projection present (else ensure_kakb)
   bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called
   bool step_timed = false;    // ev[3] recorded after this score_all's best-set detail kernel
+  bool timing = false;        // cosched_set_timing: record the prep / score split events
+  bool split_timed = false;   // this score_all recorded them
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
   Workspace ws{};
@@ -799,13 +801,10 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
                    prep_events ? h->evp[2] : nullptr);
     h->launches += 3;
   }
-  // prep / score split for cosched_last_timings (COSCHED_NO_EV1=1: not recorded,
-  // A/B of whether an event between the gather and the scorer costs the PDL overlap)
-  static const bool no_ev1 = [] {
-    const char* e = getenv("COSCHED_NO_EV1");
-    return e && e[0] == '1';
-  }();
-  if (!no_ev1) cudaEventRecord(h->ev[1], st);
+  // prep / score split for cosched_last_timings, only when asked for
+  // (cosched_set_timing): an event between the gather and the scorer stops the
+  // scorer's launch from overlapping the gather's tail (PDL) -- 5-6 us a step
+  if (h->timing) cudaEventRecord(h->ev[1], st);
   if (h->sp.search_mode == 1) {
     launch_fill_u64((unsigned long long*)(ws.counters + 7), 0ull, 1, st);
     h->launches += 1 + launch_score_hill(h->sp, n_jobs, ws.ka, ws.kb, ws.w, first, count, obj, cfg, ws.best_key,
@@ -828,11 +827,12 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
                                 ws.err, h->variant, st, rb, pm);
   }
-  cudaEventRecord(h->ev[2], st);
+  if (h->timing) cudaEventRecord(h->ev[2], st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(h, e, "score_all launch");
   h->scored = true;
   h->step_timed = false;
+  h->split_timed = h->timing;
   h->n_jobs = n_jobs;
   h->first = first;
   h->n_sets = count;
@@ -864,9 +864,16 @@ static cosched_status deferred_status(cosched_t h, unsigned long long e) {
   return fail(h, (cosched_status)code, buf);
 }
 
+cosched_status cosched_set_timing(cosched_t h, int on) {
+  if (!h) return COSCHED_E_ARG;
+  h->timing = on != 0;
+  return COSCHED_OK;
+}
+
 cosched_status cosched_last_timings(cosched_t h, float* ms3) {
   if (!h || !ms3) return fail(h, COSCHED_E_ARG, "null argument");
   if (!h->scored) return fail(h, COSCHED_E_STATE, "call cosched_score_all first");
+  if (!h->split_timed) return fail(h, COSCHED_E_STATE, "the last cosched_score_all ran without cosched_set_timing(h, 1)");
   DeviceGuard g(h->device);
   CK(cudaEventSynchronize(h->ev[2]));
   CK(cudaEventElapsedTime(&ms3[0], h->ev[0], h->ev[1]));

@@ -6,6 +6,7 @@ import paper_2405_03838_b200 as cs
 from synth import bench_config
 pb, F = bench_config(sys.argv[1] if len(sys.argv) > 1 else "C4")
 s = cs.Scheduler(pb)
+s.set_timing(True)
 Fd = torch.from_numpy(F).cuda()
 for with_out in (True, False, True, False):
     for _ in range(3):
