@@ -120,6 +120,8 @@ struct cosched_ctx {
   bool best_pending = false;  // cosched_best_set_begin enqueued, _end not yet called
   bool step_timed = false;    // ev[3] recorded after this score_all's best-set detail kernel
   bool timing = false;        // cosched_set_timing: record the prep / score split events
+  unsigned merge_epoch = 0;   // step tag of the pair scorer's tail-merge area (PairMerge::epoch)
+  const void* merge_init = nullptr;  // workspace merge area zeroed once (its entries carry step tags after)
   bool split_timed = false;   // this score_all recorded them
   int64_t n_jobs = 0;
   int64_t first = 0, n_sets = 0;
@@ -751,6 +753,12 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
   workspace_layout(n_jobs, h->sp, count, h->comm ? h->nranks : 0, (char*)workspace_dev, &ws);
   h->sp.n_jobs_pad = pad_jobs(n_jobs);
   cudaEventRecord(h->ev[0], st);
+  if (ws.merge && ws.merge_tiles > 0 && h->merge_init != (const void*)ws.merge) {
+    // the tail-merge area keeps step-tagged entries between calls: zeroed once per workspace
+    cudaMemsetAsync(ws.merge, 0, (size_t)ws.merge_tiles * 64 * 64 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(ws.merge_cnt, 0, (size_t)ws.merge_tiles * sizeof(unsigned), st);
+    h->merge_init = ws.merge;
+  }
   launch_step_init(ws.err, ws.best_key, ws.rescore_n, ws.wmm, st);
   h->launches += 1;
   // instrumentation (COSCHED_PREP_EVENTS=1): the prep's parts, printed by
@@ -824,6 +832,9 @@ cosched_status cosched_score_all(cosched_t h, const float* features_dev, int64_t
     pm.ev_fork = h->ev_fork;
     pm.ev_join = h->ev_join;
     pm.ev_join2 = h->ev_join2;
+    h->merge_epoch = (h->merge_epoch + 1u) & 0xFFFFFFu;  // per step, never 0 (the zeroed state)
+    if (h->merge_epoch == 0u) h->merge_epoch = 1u;
+    pm.epoch = h->merge_epoch;
     h->launches += launch_score(h->sp, n_jobs, ws.ka, ws.kb, ws.w, ws.fast, first, count, obj, cfg, ws.best_key,
                                 ws.err, h->variant, st, rb, pm);
   }

@@ -82,6 +82,7 @@ struct PairMerge {
   // re-scoring pass); null = everything on the caller's stream
   cudaStream_t side = nullptr, side2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  unsigned epoch = 1;  // 24-bit step tag of the merge entries and tile counters (never 0)
 };
 
 // Device-side tables owned by a handle.

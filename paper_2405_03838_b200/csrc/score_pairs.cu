@@ -69,7 +69,30 @@ struct PairGrid {
   int n_sg;
   unsigned long long* merge;
   unsigned* cnt;  // non-null: per split tile, units done; the last unit resolves the tile (no finish launch)
+  unsigned epoch;  // 24-bit step tag of the merge entries and counters (no reset between steps)
 };
+
+// Stage-split merge entry: [step epoch : 24][best masked key bits : 32][255 - stage : 8].
+// atomicMax keeps this step's entries over any earlier step's (larger epoch), then
+// the largest key, then the lowest stage (the canonical first maximum); the merge
+// area is never reset between steps (zeroed once per workspace, api.cu).
+__device__ __forceinline__ unsigned long long merge_entry(unsigned epoch, unsigned key_bits, int stage) {
+  return ((unsigned long long)(epoch & 0xFFFFFFu) << 40) | ((unsigned long long)key_bits << 8) |
+         (unsigned long long)(255 - stage);
+}
+// Count one finished unit of a split tile, [epoch : 24][count : 8]: the first
+// unit of this step restarts the count. Returns the count after this unit.
+__device__ __forceinline__ unsigned tile_count_up(unsigned* c, unsigned epoch) {
+  const unsigned ep = epoch & 0xFFFFFFu;
+  unsigned cur = atomicAdd(c, 0u), nv;
+  while (true) {
+    nv = (cur >> 8) == ep ? cur + 1u : ((ep << 8) | 1u);
+    const unsigned prev = atomicCAS(c, cur, nv);
+    if (prev == cur) break;
+    cur = prev;
+  }
+  return nv & 0xFFu;
+}
 
 __device__ __forceinline__ void tile_coords(const PairGrid& g, int64_t t, int64_t* I, int64_t* J) {
   // tiles are ordered column tile J ascending, row tile I = 0..J; cum(J) = J(J+1)/2 - base
@@ -136,13 +159,14 @@ __device__ __forceinline__ void merge_finish_part(const SpaceParams& sp, const P
                                                   const RescoreBuf& rb, unsigned long long* mg, int64_t I, int64_t J,
                                                   int e0, float thr, unsigned long long* key);
 
+// The scorer's work for one CTA: units t0, t0 + stride, ... of the launch
+// described by g (whole tiles, stage-split units or row-group units).
 template <int MINB, int NB, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, MINB)
-    k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
-                        const float* __restrict__ fast,
-                        float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
-                        unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err,
-                        const RescoreBuf rb) {
+__device__ __forceinline__ void pairs_body(const SpaceParams& sp, const PairGrid& g, const float* __restrict__ w,
+                                           const float* __restrict__ fast, float* __restrict__ out_obj,
+                                           int32_t* __restrict__ out_cfg, unsigned long long* __restrict__ best_key,
+                                           const unsigned long long* __restrict__ err, const RescoreBuf& rb,
+                                           int64_t t0, int64_t stride) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ float s_thr;  // exact re-scoring threshold (rescore_threshold)
@@ -158,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const unsigned one = g.one;
   unsigned long long key = 0;
 
-  int64_t t = blockIdx.x;  // work unit
+  int64_t t = t0;  // work unit
   if (t >= g.n_units) {
     pdl_wait();
     if (*err == ~0ull) block_max_key(0ull, best_key);
@@ -199,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     int64_t nt = t, nI = I, nJ = J;
     int ns = s + 1, nb0 = b0, ns_lo = 0, ns_hi = 0;
     if (ns == (SPLIT ? split_stage_hi(g, sp.n_stages, t) : sp.n_stages)) {
-      nt = t + gridDim.x;
+      nt = t + stride;
       if (nt < g.n_units) unit_coords<NB, SPLIT>(g, sp.n_stages, nt, &nI, &nJ, &nb0, &ns_lo, &ns_hi);
       ns = SPLIT ? ns_lo : 0;
     }
@@ -277,8 +301,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int e = (ty + 16 * b) * kBgRow + tx + 16 * a;
         const float m = sbest[e];
         if (m > 0.0f)
-          atomicMax(mg + (ty + 16 * b) * kTile + tx + 16 * a,
-                    ((unsigned long long)__float_as_uint(m) << 32) | (0xFFFFFFFFull - (unsigned long long)(unsigned)sbg[e]));
+          atomicMax(mg + (ty + 16 * b) * kTile + tx + 16 * a, merge_entry(g.epoch, __float_as_uint(m), sbg[e]));
         sbg[e] = -1;
       }
       if (g.cnt) {
@@ -286,14 +309,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // every unit's merge atomics are visible before its count
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(g.cnt + (int)t / g.n_sg, 1u) == (unsigned)(g.n_sg - 1);
+        if (threadIdx.x == 0) s_last = tile_count_up(g.cnt + (int)t / g.n_sg, g.epoch) == (unsigned)g.n_sg;
         __syncthreads();
         if (s_last) {
           __threadfence();
 #pragma unroll 1
           for (int q = 0; q < 4; q++)
             merge_finish_part(sp, g, w, out_obj, out_cfg, rb, mg, I, J, q * (kTile * kTile / 4), s_thr, &key);
-          if (threadIdx.x == 0) g.cnt[(int)t / g.n_sg] = 0u;
         }
       }
     }
@@ -375,6 +397,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
   block_max_key(key, best_key);
 }
 
+template <int MINB, int NB, bool SPLIT>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_score_pairs_tiled(const SpaceParams sp, const PairGrid g, const float* __restrict__ w,
+                        const float* __restrict__ fast, float* __restrict__ out_obj, int32_t* __restrict__ out_cfg,
+                        unsigned long long* __restrict__ best_key, const unsigned long long* __restrict__ err,
+                        const RescoreBuf rb) {
+  pairs_body<MINB, NB, SPLIT>(sp, g, w, fast, out_obj, out_cfg, best_key, err, rb, blockIdx.x, gridDim.x);
+}
+
+
 // Resolution of the stage-split tiles (four blocks per tile): per pair the merged
 // (best masked key, first stage) gives the config -- stage and the key's low
 // bits, as in the tile end -- and the exact FP32 objective w0 + w1 of it; the
@@ -398,13 +430,12 @@ __device__ __forceinline__ void merge_finish_part(const SpaceParams& sp, const P
     const int e = e0 + u * 256 + threadIdx.x, rj = e >> 6, ri = e & 63;
     const int64_t j0 = I * kTile + ri, j1 = J * kTile + rj;
     const unsigned long long v = __ldcg(mg + e);  // L2: written by other CTAs' atomics
-    mg[e] = 0ull;  // reset for the next step
     const bool ok = j0 < j1 && j1 >= g.c0 && j1 < g.c1;
     c_[u] = ok ? -1 : -2;
     f0[u] = f1[u] = 0.0f;
-    if (ok && v) {
-      const int sg = (int)(0xFFFFFFFFull - (v & 0xFFFFFFFFull));
-      const int c = sg * kStageCfg + 31 - (int)((v >> 32) & 31u);
+    if (ok && (unsigned)(v >> 40) == (g.epoch & 0xFFFFFFu)) {  // a feasible stage group wrote it this step
+      const int sg = 255 - (int)(v & 0xFFu);
+      const int c = sg * kStageCfg + 31 - (int)((v >> 8) & 31u);
       c_[u] = c;
       const int st = (int)__fmul_rn((float)c + 0.5f, sp.inv_ncaps), p = c - st * sp.n_caps;
       f0[u] = __ldg(w + (int64_t)(st * npad + (int)j0) * rsz + p);
@@ -534,7 +565,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   // fixed cost (the merge atomics and the pipeline start, ~0.3 of a stage,
   // measured on C4); q = 1 keeps whole tiles. Ties keep fewer, larger units.
   int n_sg = 1;
-  if (R > 0 && merge.buf && minb == 2 && R <= merge.tiles) {
+  if (R > 0 && merge.buf && minb == 2 && R <= merge.tiles && sp.n_stages <= 255) {  // stage in 8 bits
     auto tail_len = [&](int q) {
       return (double)((R * q + slots - 1) / slots) * ((sp.n_stages + q - 1) / q + (q > 1 ? 0.3 : 0.0));
     };
@@ -548,6 +579,8 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   }
   const int64_t n_whole = n_sg > 1 ? n_full - R : n_full;
   int launches = 0;
+  g.epoch = merge.epoch;
+  g.cnt = nullptr;
   // partial-column units (side stream) and stage-split tail units (side2): both
   // are enqueued at once next to the whole-tile launch, so their CTAs take the
   // slots it frees in its last round (no launch gap); the tail units resolve
@@ -556,7 +589,6 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
   const char* tc = getenv("COSCHED_PAIR_TAIL_CONC");
   const bool conc = n_sg > 1 && !(tc && tc[0] == '0') && merge.side2 && merge.cnt && merge.ev_join2 && merge.ev_fork;
   const bool fork_side = n_seg > 0 && merge.side && merge.ev_fork && merge.ev_join;
-  g.cnt = nullptr;
   if (fork_side || conc) cudaEventRecord(merge.ev_fork, st);
   cudaStream_t ust = st, sst = st;
   if (fork_side) {
@@ -581,9 +613,7 @@ int launch_score_pairs_fast(const SpaceParams& sp, int64_t n_jobs, const float* 
                  cfg, best_key, err, rb);
   }
   if (n_sg > 1) {
-    launches += conc ? 2 : 3;
-    cudaMemsetAsync(merge.buf, 0, (size_t)R * kTile * kTile * sizeof(unsigned long long), sst);
-    if (conc) cudaMemsetAsync(merge.cnt, 0, (size_t)R * sizeof(unsigned), sst);
+    launches += conc ? 1 : 2;  // the merge entries and tile counts carry the step's epoch: no reset
     g.t0 = fa + n_whole;
     g.n_units = R * n_sg;
     g.n_sg = n_sg;
