@@ -181,7 +181,13 @@ cosched_status cosched_workspace_size(cosched_t h, int64_t n_jobs, size_t* bytes
  *  features_dev: float [n_rows][8], counters F1..F8 in percent (Table `counters`)
  *  jobs_dev:     int32 [n_jobs] row of each queue position, or NULL for row = position
  *  n_rows:       rows of features_dev (validates jobs_dev)
- *  workspace_dev: >= cosched_workspace_size bytes, 256-byte aligned
+ *  workspace_dev: >= cosched_workspace_size bytes, 256-byte aligned; device
+ *                memory the handle uses between its calls (later calls read
+ *                this call's results from it). One region of it, the pair
+ *                scorer's stage-split merge area, keeps step-tagged entries from
+ *                call to call: it is zeroed the first time a handle sees a
+ *                workspace pointer, so pass a new pointer (or a new handle) after
+ *                writing to the workspace yourself
  *  out:          host struct with device pointers (may be NULL)
  * Steps (all kernels): validate features (E_RANGE / E_DEGENERATE_PROFILE for
  * the first bad queue position, reported at the next synchronising call),
