@@ -63,21 +63,17 @@ __global__ void k_obj_minmax(const float* __restrict__ obj, int64_t count, unsig
   }
 }
 
-// Bins: kHistBins = 2^14 equal slices of [lo, hi] in ord(obj) space, bin(u) =
-// floor((u - lo) 2^14 / (span + 1)). Its first value t(b) = lo + ceil(b (span + 1)
-// / 2^14) needs only a multiply and a shift, so a bin range is a range of u and
-// the per-element bin is a floating-point estimate corrected against t (no
-// 64-bit division on the hot path).
-__device__ __forceinline__ unsigned long long bin_start(unsigned lo, unsigned span, int b) {
-  return (unsigned long long)lo +
-         (((unsigned long long)b * ((unsigned long long)span + 1ull) + ((1ull << kHistLog2) - 1ull)) >> kHistLog2);
+// Bins: 2^14 bins of 2^k ord(obj) units each from lo, k the smallest shift
+// with ceil((span + 1) / 2^k) <= 2^14: bin(u) = (u - lo) >> k, a bin range is a
+// range of u, and binning an element is a subtraction and a shift (the
+// histogram pass streams the whole objective array at HBM speed).
+__host__ __device__ __forceinline__ int hist_shift(unsigned span) {
+  int k = 0;
+  while ((((unsigned long long)span + 1ull + (1ull << k) - 1ull) >> k) > (unsigned long long)kHistBins) k++;
+  return k;
 }
-__device__ __forceinline__ int bin_of(unsigned u, unsigned lo, unsigned span, double scale) {
-  int b = (int)((double)(u - lo) * scale);
-  b = b < 0 ? 0 : (b > kHistBins - 1 ? kHistBins - 1 : b);
-  while (b < kHistBins - 1 && bin_start(lo, span, b + 1) <= u) b++;
-  while (b > 0 && bin_start(lo, span, b) > u) b--;
-  return b;
+__device__ __forceinline__ unsigned long long bin_start(unsigned lo, unsigned span, int b) {
+  return (unsigned long long)lo + ((unsigned long long)b << hist_shift(span));
 }
 
 // ---- greedy-list keys (cosched_internal.h GKeyFmt) ----
@@ -93,10 +89,8 @@ GKeyFmt gkey_format(int n_slots, int64_t n_jobs, unsigned base, unsigned long lo
 }
 
 void bin_range_ord(unsigned lo, unsigned hi, int bin_lo, int bin_hi, unsigned* u_lo, unsigned long long* width) {
-  const unsigned long long span = (unsigned long long)(hi - lo);
-  auto start = [&](int b) {
-    return (unsigned long long)lo + (((unsigned long long)b * (span + 1ull) + ((1ull << kHistLog2) - 1ull)) >> kHistLog2);
-  };
+  const int k = hist_shift(hi - lo);
+  auto start = [&](int b) { return (unsigned long long)lo + ((unsigned long long)b << k); };
   *u_lo = (unsigned)start(bin_lo);
   *width = start(bin_hi + 1) - start(bin_lo);
 }
@@ -137,11 +131,11 @@ __global__ void __launch_bounds__(1024) k_obj_hist(const float* __restrict__ obj
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) s_hist[i] = 0u;
   __syncthreads();
   const unsigned lo = mm[0], span = mm[1] - mm[0];
-  const double scale = (double)kHistBins / ((double)span + 1.0);
+  const int sh = hist_shift(span);
   const int64_t n4 = vec4_count(obj, count), stride = (int64_t)gridDim.x * blockDim.x;
   const float4* o4 = reinterpret_cast<const float4*>(obj);
   auto take = [&](float o) {
-    if (o > -INFINITY) atomicAdd(&s_hist[bin_of(ord_float_d(o), lo, span, scale)], 1u);
+    if (o > -INFINITY) atomicAdd(&s_hist[(ord_float_d(o) - lo) >> sh], 1u);
   };
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4; k += stride) {
     const float4 v = __ldcs(o4 + k);
