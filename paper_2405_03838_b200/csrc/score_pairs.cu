@@ -25,10 +25,15 @@
 //    candidate, FMA pipe 2 -- the mix that measured fastest in
 //    tools/microbench/inner.cu;
 //  - per stage and pair one FSETP + 2 predicated moves; per tile and pair the
-//    exact FP32 objective of the chosen config (2 loads + 1 FADD);
-//  - the last round's tiles (n_tiles mod CTA slots) can go to a second launch
-//    as 2 or 4 units of 16-row j1 groups each (k_score_pairs_tiled<MINB, NB>),
-//    chosen to minimise the tail's length.
+//    exact FP32 objective of the chosen config (2 loads + 1 FADD), resolved by
+//    the thread that owns the pair with all its loads in flight (tile end);
+//  - the last round's tiles (whole tiles mod CTA slots) are split along the
+//    config axis into stage-group units (k_score_pairs_tiled<2, 4, true>) on a
+//    side stream, enqueued next to the whole-tile launch; the last unit of a tile
+//    resolves it from the step-tagged merge entries; the queue's ragged last
+//    column block runs as 16-row units (<2, 1, false>) on another side stream;
+//  - the whole-tile launch is PDL-launched behind the gather (its prologue
+//    overlaps the gather's tail).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
