@@ -67,3 +67,28 @@ def test_last_step_ms_brackets_the_step(cs):
     e1.synchronize()
     inner, outer = s.last_step_ms(), e0.elapsed_time(e1)
     assert 0.0 < inner <= outer + 1e-3
+
+
+def test_consecutive_steps_on_one_handle_match_fresh_handles(cs):
+    """The pair scorer's stage-split merge area keeps step-tagged entries between
+    calls (never reset): back-to-back queues on one handle -- with tail tiles, the
+    second queue having pairs infeasible where the first had feasible ones -- must
+    give exactly what fresh handles give."""
+    pb = make_problem("b200", "c21", coef_seed=97, alpha=0.6)
+    F1, _ = make_features(2000, seed=97)   # 32 column blocks: 528 tiles, a stage-split tail
+    F2, _ = make_features(2000, seed=98)
+    shared = cs.Scheduler(pb)
+    for F in (F1, F2, F1):
+        Fd = torch.from_numpy(F).cuda()
+        o1, c1 = shared.score_all(Fd)
+        o1, c1 = o1.cpu().numpy().copy(), c1.cpu().numpy().copy()
+        fresh = cs.Scheduler(pb)
+        o2, c2 = fresh.score_all(Fd)
+        assert np.array_equal(c1, c2.cpu().numpy())
+        assert np.array_equal(o1, o2.cpu().numpy())
+        assert shared.best_set() == fresh.best_set()
+    # the two queues really differ in feasibility somewhere (the stale-entry case)
+    Fa, Fb = torch.from_numpy(F1).cuda(), torch.from_numpy(F2).cuda()
+    _, ca = cs.Scheduler(pb).score_all(Fa)
+    _, cb = cs.Scheduler(pb).score_all(Fb)
+    assert ((ca.cpu().numpy() >= 0) != (cb.cpu().numpy() >= 0)).any()
