@@ -92,3 +92,23 @@ def test_consecutive_steps_on_one_handle_match_fresh_handles(cs):
     _, ca = cs.Scheduler(pb).score_all(Fa)
     _, cb = cs.Scheduler(pb).score_all(Fb)
     assert ((ca.cpu().numpy() >= 0) != (cb.cpu().numpy() >= 0)).any()
+
+
+def test_prep_scorer_split_only_on_request(cs):
+    """cosched_last_timings needs cosched_set_timing(h, 1) for that step (its events
+    cost the PDL overlap, so the default step records none)."""
+    pb, F = bench_config("C3")
+    s = cs.Scheduler(pb)
+    Fd = torch.from_numpy(F).cuda()
+    s.score_all(Fd)
+    with pytest.raises(cs.CoschedError) as e:
+        s.last_timings()
+    assert cs.STATUS[e.value.status] == "E_STATE"
+    s.set_timing(True)
+    s.score_all(Fd)
+    prep, score, total = s.last_timings()
+    assert 0.0 < prep < total and 0.0 < score < total and prep + score <= total + 1e-3
+    s.set_timing(False)
+    s.score_all(Fd)
+    with pytest.raises(cs.CoschedError):
+        s.last_timings()
