@@ -176,37 +176,6 @@ __device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
 // completion and memory; allow the successor to launch
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-// L2 cache policies (createpolicy): evict_last for small operand tables read
-// over and over while a large output stream passes through L2, evict_first for
-// that write-once stream
-__device__ __forceinline__ uint64_t l2_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_evict_normal() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ float ldg_l2hint(const float* a, uint64_t pol) {
-  float v;
-  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_l2hint(float* a, float v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_l2hint(int32_t* a, int32_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
-}
-// C(n, 2) mod 2^31 (n(n-1) is even): enough for the low address bits of a colex run
-__device__ __forceinline__ unsigned c2i(int n) { return ((unsigned)n * (unsigned)(n - 1)) >> 1; }
 __device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
 
 // colex unranking: set id -> ascending queue positions. FP32 root estimates

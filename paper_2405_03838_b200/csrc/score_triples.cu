@@ -322,27 +322,8 @@ __global__ void __launch_bounds__(kTThreads, MINB)
           const float bo = bc >= 0 ? __fadd_rn(f0[u], __fadd_rn(f1[u], f2[u])) : -INFINITY;
           const int64_t sid = sid2 + (((int64_t)j1 * (j1 - 1)) >> 1) + j0;
           const int64_t k = sid - g.first_set;
-#ifdef COSCHED_L2HINT_ST
-          // this tile's run of row (j1, j2) is [k0, k0 + len); a 32-byte sector that
-          // also holds outputs of a neighbouring run is written in two parts, often
-          // a whole round apart: keep it in L2 (evict_last) until both parts land,
-          // so it is never evicted half-written (a DRAM read-modify-write)
-          const int64_t k0 = sid2 + (((int64_t)j1 * (j1 - 1)) >> 1) + jA - g.first_set;
-          const int len = min(kTT, j1 - jA);
-          const int64_t ka = k + (int64_t)((((uintptr_t)out_obj) >> 2) & 7);  // sector-relative index
-          const int64_t ka0 = k0 + (int64_t)((((uintptr_t)out_obj) >> 2) & 7);
-          const bool shared_sector = ((ka & ~7ll) < ka0) || ((ka | 7ll) >= ka0 + len);
-#ifdef COSCHED_L2HINT_NORMAL
-          const uint64_t pol = shared_sector ? l2_evict_last() : l2_evict_normal();
-#else
-          const uint64_t pol = shared_sector ? l2_evict_last() : l2_evict_first();
-#endif
-          if (out_obj) st_l2hint(out_obj + k, bo, pol);
-          if (out_cfg) st_l2hint(out_cfg + k, bc, pol);
-#else
           if (out_obj) out_obj[k] = bo;
           if (out_cfg) out_cfg[k] = bc;
-#endif
           if (bc >= 0) {
             const unsigned long long kk = pack_key(bo, sid);
             key = kk > key ? kk : key;
