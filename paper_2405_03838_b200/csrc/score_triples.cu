@@ -48,6 +48,7 @@ struct TripleGrid {
   int64_t n_tiles;
   int64_t first_set;
   unsigned one;    // runtime 1 for IMAD
+  int pair_major;  // tile order (ttile_coords): 1 block pair major (default), 0 plane major
 };
 
 // tiles of the planes j2' < j2: plane j has B(j) = ceil(j/64) j1-blocks and B(B+1)/2 tiles
@@ -57,7 +58,7 @@ __host__ __device__ __forceinline__ int64_t tiles_before(int64_t j2) {
   return 32 * n * (n + 1) * (n + 2) / 3 + rem * (n + 1) * (n + 2) / 2;
 }
 
-__device__ __forceinline__ void ttile_coords(const TripleGrid& g, int64_t t, int64_t* j2, int64_t* b, int64_t* a) {
+__device__ __forceinline__ void ttile_coords_planes(const TripleGrid& g, int64_t t, int64_t* j2, int64_t* b, int64_t* a) {
   int64_t lo = g.c0, hi = g.c1 - 1;  // largest plane with tiles_before(plane) - cum0 <= t
   while (lo < hi) {
     int64_t mid = (lo + hi + 1) / 2;
@@ -71,6 +72,35 @@ __device__ __forceinline__ void ttile_coords(const TripleGrid& g, int64_t t, int
   while ((bb + 1) * (bb + 2) / 2 <= u) bb++;
   *b = bb;
   *a = u - bb * (bb + 1) / 2;
+}
+
+// Tile order: block pair (b, a) major, the rank's planes j2 inner -- tiles
+// running at the same time read the same (a, b) operand blocks of the gathered
+// layout (1.8 MB of TMA source for all 45 stages) and differ only in their
+// single j2 rows, so the operands stay in L2 under the 10.65 GB output stream
+// (plane-major order cycled the whole 177 MB layout through L2). Plane j2 has
+// tiles (a <= b) for b < ceil(j2 / 64), i.e. j2 > 64 b.
+__device__ __forceinline__ void ttile_coords(const TripleGrid& g, int64_t t, int64_t* j2, int64_t* b, int64_t* a) {
+  if (g.pair_major) {
+    for (int64_t bb = 0;; bb++) {
+      const int64_t lo = g.c0 > 64 * bb + 1 ? g.c0 : 64 * bb + 1;
+      const int64_t n = g.c1 > lo ? g.c1 - lo : 0;  // planes with block bb
+      const int64_t cnt = (bb + 1) * n;
+      if (t < cnt) {
+        *b = bb;
+        if (g.pair_major == 2) {  // b, then j2, then a: a row's runs (all a) are written together
+          *a = t % (bb + 1);
+          *j2 = lo + t / (bb + 1);
+        } else {
+          *a = t / n;
+          *j2 = lo + t % n;
+        }
+        return;
+      }
+      t -= cnt;
+    }
+  }
+  ttile_coords_planes(g, t, j2, b, a);
 }
 
 // Stage (floats): role blocks 0..7 of kTT rows x kStageRS (j0 rows for roles
@@ -376,6 +406,8 @@ int launch_score_triples_fast(const SpaceParams& sp, int64_t n_jobs, const float
   g.one = 1u;
   g.cum0 = tiles_before(c0);
   g.n_tiles = tiles_before(c1) - g.cum0;
+  const char* to = getenv("COSCHED_TRIPLE_ORDER");  // A/B: 0 = r01 plane major, 1 = (b, a, j2), 2 = (b, j2, a)
+  g.pair_major = to ? atoi(to) : 2;
   constexpr size_t smem = (size_t)2 * (8 * kTT * kStageRS + 4 * kStageRS) * sizeof(float) +
                           (size_t)kTT * kTBgRow * (sizeof(float) + sizeof(int16_t));
   const char* mb = getenv("COSCHED_TRIPLE_MINB");
